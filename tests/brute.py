@@ -1,0 +1,353 @@
+"""Brute-force / exact-rational re-derivations used to PIN the oracle (test code only).
+
+Written directly from PAPER.md, independently of oracle/oracle.c:
+  * enumerate(): the canonical index order by itertools (no unranking arithmetic);
+  * exact(): Table 2 per-iteration terms with per-layer sums in fractions.Fraction;
+  * ring_allreduce_sim / ring_allgather_sim: explicit ring data movement;
+  * gpipe_makespan: discrete-event GPipe schedule;
+  * buffer_bytes: enumeration of every per-layer buffer.
+"""
+from __future__ import annotations
+
+import itertools
+from fractions import Fraction as Fr
+from math import prod
+
+from workloads import models as M
+from workloads import sweeps as W
+
+R_SCALING, R_MEMORY, R_SPLIT, R_TIER, R_SEGMENTS = 1, 2, 4, 8, 16
+
+
+# ------------------------------------------------------------------ enumeration
+def partitions(G, sub):
+    if sub.family not in W.PIPE_FAMILIES:
+        return [(G,)]
+    if sub.part_mode == W.PART_MASK:
+        out = []
+        for mask in range(1 << (G - 1)):
+            ends = [j + 1 for j in range(G - 1) if (mask >> j) & 1] + [G]
+            out.append(tuple(ends))
+        return out
+    out = []
+    for s in range(sub.s_min, sub.s_max + 1):
+        for cuts in itertools.combinations(range(1, G), s - 1):
+            out.append(tuple(cuts) + (G,))
+    return out
+
+
+def enumerate_configs(sweep):
+    """Yield (idx, cfg dict) in canonical order: cap, flops, b, partition, S, dims, Ls, alpha, beta."""
+    sys = sweep.system
+    idx = 0
+    for si, sub in enumerate(sweep.subs):
+        m = sweep.models[sub.model]
+        caps = sub.cap or [sys.hbm_bytes]
+        flops = sub.flops or [sys.flops_per_s]
+        Ss = sub.S or [1]
+        dimss = sub.dims or [(1, 1, 1, 1)]
+        Lss = sub.Ls or [0]
+        alphas = sub.alpha or [[t.alpha for t in sys.tiers]]
+        betas = sub.beta or [[t.beta for t in sys.tiers]]
+        parts = partitions(m.G, sub)
+        for cap, R, b, part, S, dims, Ls, a, bb in itertools.product(
+                caps, flops, sub.b, parts, Ss, dimss, Lss, alphas, betas):
+            yield idx, dict(sub=si, family=sub.family, model=sub.model, cap=cap, R=R, b=b,
+                            ends=part, S=S, dims=dims, Ls=Ls, alpha=a, beta=bb)
+            idx += 1
+
+
+# ------------------------------------------------------------------ exact evaluation
+def tier_of(sys, span):
+    for t, tr in enumerate(sys.tiers):
+        if tr.max_pes >= span:
+            return t
+    return None
+
+
+def _ceil(a, b):
+    return -(-a // b)
+
+
+def halo_rows(layer, split, which):
+    """halo(x) (which=0) / halo(dL/dy) (which=1) of one row, elements per sample (Q15)."""
+    tot = 0
+    for a in range(3):
+        if split[a] <= 1:
+            continue
+        h = layer.K[a] // 2
+        if h == 0:
+            continue
+        ext = layer.X if which == 0 else layer.Y
+        ch = layer.C if which == 0 else layer.F
+        cross = prod(_ceil(ext[o], split[o]) for o in range(3) if o != a)
+        tot += ch * h * cross * (2 if split[a] > 2 else 1)
+    return tot
+
+
+def ar_exact(sys, n, m, seg, alpha, beta):
+    if n == 1:
+        return Fr(0)
+    if sys.tree_threshold > 0 and m < Fr(sys.tree_threshold):
+        lg = 0
+        while (1 << lg) < n:
+            lg += 1
+        return 2 * (lg + sys.tree_chunks) * (alpha + m / (2 * sys.tree_chunks) * beta)
+    return 2 * (n - 1) * (alpha + seg * beta)
+
+
+def exact(sweep, cfg):
+    """Per-iteration Table 2 terms in exact rationals with literal per-layer sums."""
+    sys = sweep.system
+    m = sweep.models[cfg["model"]]
+    L = m.layers
+    fam = cfg["family"]
+    b = cfg["b"]
+    tau = Fr(1) / Fr(cfg["R"])
+    dl = sys.delta
+    A = [Fr(v) for v in cfg["alpha"]]
+    Bt = [Fr(v) for v in cfg["beta"]]
+    gamma = Fr(sys.gamma)
+    p1, d1, d2, d3 = cfg["dims"]
+    reason = 0
+    comp = ge = ag = ar = halo = p2p = Fr(0)
+    inf = None
+
+    comm_rows = [l for l, r in enumerate(L) if r.flags & M.FLAG_COMM]
+    Cm = comm_rows[:-1]
+    FW = sum(r.fw for r in L)
+    BW = sum(r.bw for r in L)
+
+    def comp_row(Bc, pc, pu):
+        return Fr(Bc, pc) * (FW + BW) * tau + Fr(sum(r.wu for r in L), pu) * tau
+
+    def mem_row(Bm, pa, pw):
+        return gamma * dl * sum(Fr(2 * Bm * (r.x + r.y), pa) + Fr(2 * r.w, pw) + r.bi for r in L)
+
+    def tier(span):
+        nonlocal reason
+        t = tier_of(sys, span)
+        if t is None:
+            reason |= R_TIER
+        return t
+
+    W_ = sum(r.w for r in L)
+    if fam == W.SERIAL:
+        B, p = b, 1
+        comp = comp_row(B, 1, 1)
+        mem = mem_row(B, 1, 1)
+    elif fam == W.DATA:
+        p = p1
+        B = b * p
+        comp = comp_row(B, p, 1)
+        t = tier(p)
+        ge = inf if t is None else ar_exact(sys, p, Fr(dl * W_), Fr(dl * W_, p), A[t], Bt[t])
+        mem = mem_row(B, p, 1)
+        if p > B:
+            reason |= R_SCALING
+    elif fam in (W.SPATIAL, W.DS):
+        split = (d1, d2, d3)
+        p2 = d1 * d2 * d3
+        p = p1 * p2
+        B = b * p1
+        comp = comp_row(B, p, 1)
+        Sp = [r for l, r in enumerate(L) if l < cfg["Ls"] and r.kind in (M.CONV, M.POOL)]
+        for r in Sp:
+            for a in range(3):
+                if split[a] <= 1:
+                    continue
+                if split[a] > r.X[a]:
+                    reason |= R_SCALING
+                h = r.K[a] // 2
+                if _ceil(r.X[a], split[a]) < h or _ceil(r.Y[a], split[a]) < h:
+                    reason |= R_SPLIT
+        ti, to = tier(p2), tier(p)
+        if p2 > 1:
+            halo = inf if ti is None else 2 * sum(
+                2 * A[ti] + b * dl * Bt[ti] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
+        if fam == W.SPATIAL:
+            ge = inf if to is None else ar_exact(sys, p, Fr(dl * W_), Fr(dl * W_, p), A[to], Bt[to])
+        else:
+            rl = inf if ti is None else ar_exact(sys, p2, Fr(dl * W_), Fr(dl * W_, p2), A[ti], Bt[ti])
+            al = inf if to is None else ar_exact(sys, p1, Fr(dl * W_), Fr(dl * W_, p1), A[to], Bt[to])
+            ge = inf if (rl is None or al is None) else rl + al
+        mem = mem_row(B, p, 1)
+    elif fam in (W.FILTER, W.CHANNEL):
+        p = p1
+        B = b
+        comp = comp_row(B, p, p)
+        t = tier(p)
+        if p > 1:
+            ag = inf if t is None else (p - 1) * sum(A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm)
+            ar = inf if t is None else 2 * (p - 1) * sum(A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm)
+        mem = mem_row(B, 1, p)
+        if fam == W.FILTER:
+            lim = min((L[l].F for l in comm_rows), default=None)
+        else:
+            lim = min((L[l].C for l in comm_rows[1:]), default=None)
+        if lim is not None and p > lim:
+            reason |= R_SCALING
+    elif fam == W.DF:
+        p2 = d1
+        p = p1 * p2
+        B = b * p1
+        comp = comp_row(B, p, p2)
+        ti, to = tier(p2), tier(p)
+        if p2 > 1:
+            ag = inf if ti is None else (p2 - 1) * sum(A[ti] + Fr(B * L[l].y, p) * dl * Bt[ti] for l in Cm)
+            ar = inf if ti is None else 2 * (p2 - 1) * sum(A[ti] + Fr(B * L[l].y, p) * dl * Bt[ti] for l in Cm)
+        phi = Fr(sys.phi_df) if p2 > 1 else Fr(1)
+        if to is None:
+            ge = inf if p1 > 1 else Fr(0)
+        else:
+            ge = ar_exact(sys, p1, Fr(dl * W_, p2), Fr(dl * W_, p), A[to], Bt[to] * phi)
+        mem = mem_row(B, p1, p2)
+        lim = min((L[l].F for l in comm_rows), default=None)
+        if lim is not None and p2 > lim:
+            reason |= R_SCALING
+    else:
+        ends = cfg["ends"]
+        s = len(ends)
+        S = cfg["S"]
+        pd = p1 if fam == W.PD else 1
+        p = s * pd
+        B = b * pd
+        groups = []
+        beg = 0
+        for e in ends:
+            groups.append(L[beg:e])
+            beg = e
+        FWg = [sum(r.fw for r in g) * tau for g in groups]
+        BWg = [sum(r.bw for r in g) * tau for g in groups]
+        WUg = [sum(r.wu for r in g) * tau for g in groups]
+        Wg = [sum(r.w for r in g) for g in groups]
+        ycut = [g[-1].y for g in groups[:-1]]
+        ts = tier(s)
+        if fam == W.LAYERPURE:
+            comp = comp_row(b, 1, 1)
+            if s > 1:
+                p2p = inf if ts is None else 2 * sum(A[ts] + dl * b * y * Bt[ts] for y in ycut)
+        else:
+            comp = Fr(s + S - 1, S) * b * (max(FWg) + max(BWg)) + max(WUg)
+            if s > 1:
+                p2p = inf if ts is None else 2 * (s + S - 2) * max(A[ts] + Fr(b, S) * y * dl * Bt[ts] for y in ycut)
+            if fam == W.PD:
+                tp = tier(p)
+                if tp is None:
+                    ge = inf if pd > 1 else Fr(0)
+                else:
+                    mW = dl * max(Wg)
+                    ge = ar_exact(sys, pd, Fr(mW), Fr(mW, pd), A[tp], Bt[tp])
+        mem = gamma * dl * max(sum(2 * b * (r.x + r.y) + 2 * r.w + r.bi for r in g) for g in groups)
+        if S < 1 or S > b:
+            reason |= R_SEGMENTS
+    terms = [comp, ge, ag, ar, halo, p2p]
+    t_iter = None if any(v is None for v in terms) else sum(terms)
+    if not (mem <= Fr(cfg["cap"])):
+        reason |= R_MEMORY
+    I = Fr(m.D, B)
+    return dict(t_comp=comp, t_ge=ge, t_fb_ag=ag, t_fb_ar=ar, t_halo=halo, t_p2p=p2p,
+                t_iter=t_iter, I=I, t_epoch=None if t_iter is None else t_iter * I,
+                mem=mem, reason=reason, B=B, p=p)
+
+
+# ------------------------------------------------------------------ simulators
+def ring_allreduce_sim(p, m, alpha, beta):
+    """Explicit ring reduce-scatter + allgather over p PEs of an m-byte buffer in p chunks
+    (P:553-555).  Returns (time, final buffers) with exact rationals."""
+    if p == 1:
+        return Fr(0), None
+    seg = Fr(m, p)
+    # data[i][c] = contribution of PE i to chunk c (use distinct primes to check the sum)
+    vals = [[(i + 1) * 1000 + c for c in range(p)] for i in range(p)]
+    acc = [list(v) for v in vals]
+    t = Fr(0)
+    for step in range(p - 1):            # reduce-scatter
+        sends = [(i, (i - step) % p, acc[i][(i - step) % p]) for i in range(p)]
+        for i, c, v in sends:
+            acc[(i + 1) % p][c] += v
+        t += alpha + seg * beta
+    owner = {}
+    for i in range(p):
+        owner[(i + 1) % p] = (i + 1) % p
+    for step in range(p - 1):            # allgather
+        sends = [(i, (i + 1 - step) % p, acc[i][(i + 1 - step) % p]) for i in range(p)]
+        for i, c, v in sends:
+            acc[(i + 1) % p][c] = v
+        t += alpha + seg * beta
+    return t, acc
+
+
+def ring_allgather_sim(p, m_seg, alpha, beta):
+    if p == 1:
+        return Fr(0)
+    have = [{i} for i in range(p)]
+    t = Fr(0)
+    for step in range(p - 1):
+        sends = [(i, (i - step) % p) for i in range(p)]
+        for i, c in sends:
+            assert c in have[i]
+            have[(i + 1) % p].add(c)
+        t += alpha + Fr(m_seg) * beta
+    assert all(len(h) == p for h in have)
+    return t
+
+
+def gpipe_makespan(fw_stage, bw_stage, S, seg_samples):
+    """Discrete-event GPipe schedule: forward wave of S segments through the stages, then
+    the backward wave in reverse stage order.  Times per segment = samples x
+    per-sample stage time."""
+    s = len(fw_stage)
+    done = [[Fr(0)] * S for _ in range(s)]
+    free = [Fr(0)] * s
+    for j in range(S):
+        for i in range(s):
+            start = max(free[i], done[i - 1][j] if i > 0 else Fr(0))
+            done[i][j] = start + seg_samples * fw_stage[i]
+            free[i] = done[i][j]
+    t_fwd = max(free)
+    bdone = [[Fr(0)] * S for _ in range(s)]
+    bfree = [t_fwd] * s
+    for j in range(S):
+        for i in reversed(range(s)):
+            start = max(bfree[i], bdone[i + 1][j] if i < s - 1 else t_fwd)
+            bdone[i][j] = start + seg_samples * bw_stage[i]
+            bfree[i] = bdone[i][j]
+    return max(bfree)
+
+
+def buffer_bytes(sweep, cfg):
+    """Enumerate every buffer one PE holds (input, activation, their gradients, weights,
+    weight gradients, bias -- P:538 / P:942) with its sharded size; sum x delta x gamma."""
+    sys = sweep.system
+    L = sweep.models[cfg["model"]].layers
+    fam = cfg["family"]
+    b = cfg["b"]
+    p1, d1, d2, d3 = cfg["dims"]
+    dl = sys.delta
+
+    def layer_bufs(r, act_samples, act_div, w_div):
+        bufs = [Fr(act_samples * r.x, act_div), Fr(act_samples * r.y, act_div),      # x, y
+                Fr(act_samples * r.x, act_div), Fr(act_samples * r.y, act_div),      # dL/dx, dL/dy
+                Fr(r.w, w_div), Fr(r.w, w_div), Fr(r.bi)]                            # w, dL/dw, bi
+        return sum(bufs)
+
+    if fam == W.SERIAL:
+        tot = sum(layer_bufs(r, b, 1, 1) for r in L)
+    elif fam == W.DATA:
+        tot = sum(layer_bufs(r, b * p1, p1, 1) for r in L)          # B' = B/p samples
+    elif fam in (W.SPATIAL, W.DS):
+        p2 = d1 * d2 * d3
+        tot = sum(layer_bufs(r, b * p1, p1 * p2, 1) for r in L)     # spatial shard of the group batch
+    elif fam in (W.FILTER, W.CHANNEL):
+        tot = sum(layer_bufs(r, b, 1, p1) for r in L)               # full activations, w/p
+    elif fam == W.DF:
+        tot = sum(layer_bufs(r, b * p1, p1, d1) for r in L)
+    else:
+        groups = []
+        beg = 0
+        for e in cfg["ends"]:
+            groups.append(L[beg:e])
+            beg = e
+        tot = max(sum(layer_bufs(r, b, 1, 1) for r in g) for g in groups)
+    return Fr(sys.gamma) * dl * tot

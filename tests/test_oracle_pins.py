@@ -1,0 +1,507 @@
+"""Pin the CPU oracle to things other than itself (CPU only, -m "not gpu").
+
+Sources of truth: worked examples re-derived from the paper's equations
+(tests/golden/spec_examples.json), values the paper prints (tests/golden/paper_pins.json),
+brute-force simulators and an exact-rational evaluator (tests/brute.py), closed-form
+invariants, and degenerate identities (SPEC S:437 / S:611-612).
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import math
+import os
+import random
+from fractions import Fraction as Fr
+
+import pytest
+
+import brute
+import toys
+from workloads import corpus
+from workloads import models as M
+from workloads import sweeps as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+EX = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+PIN = json.load(open(os.path.join(GOLD, "paper_pins.json")))
+
+
+def _one(O, model, system, sub, idx=0, fold=False):
+    sw = toys.sweep(model, system, [sub])
+    o = O.OracleSweep(sw)
+    return o.explain(idx, fold=fold)
+
+
+def _rel(a, b):
+    a, b = float(a), float(b)
+    if a == b:
+        return 0.0
+    return abs(a - b) / max(abs(a), abs(b))
+
+
+# ------------------------------------------------------------ collective primitives
+def test_allreduce_ring_example(oracle_mod):
+    e = EX["allreduce_ring"]
+    # data(p) GE = AR(p, delta*W): a single weighted row with w = m, delta = 1
+    m = toys.model([toys.row(w=e["m"])])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"]),
+              W.SubSweep(W.DATA, b=[1], dims=[(e["p"], 1, 1, 1)]))
+    assert pr.t_ge == e["expect"]
+
+
+def test_allgather_ring_example(oracle_mod):
+    # filter(p) Allgather phase = (p-1)(NC alpha + (B delta YC / p) beta): choose NC = 1,
+    # B*YC/p = m_seg  ->  rows: one comm row with y = m_seg * p, then a last comm row.
+    e = EX["allgather_ring"]
+    p = e["p"]
+    m = toys.model([toys.row(y=e["m_seg"] * p, F=64), toys.row(F=64)])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"]),
+              W.SubSweep(W.FILTER, b=[1], dims=[(p, 1, 1, 1)]))
+    assert pr.t_fb_ag == e["expect"]
+    assert pr.t_fb_ar == 2 * e["expect"]
+
+
+@pytest.mark.parametrize("case", EX["allreduce_tree"]["cases"])
+def test_allreduce_tree_examples(oracle_mod, case):
+    p, k, a, b, mbytes, expect = case
+    m = toys.model([toys.row(w=mbytes)])
+    sysd = toys.system(alpha=a, beta=b, tree_threshold=1e9, tree_chunks=k)
+    pr = _one(oracle_mod, m, sysd, W.SubSweep(W.DATA, b=[1], dims=[(p, 1, 1, 1)]))
+    assert pr.t_ge == expect
+
+
+def test_reduce_to_leader_and_ds_ge(oracle_mod):
+    e = EX["ds_ge_iter"]
+    # ds(p1; p2,1,1) GE = RL(p2, dW) + AR(p1, dW); one 1x1 row so the halo is latency-only
+    m = toys.model([toys.row(w=e["dW"], X=(64, 1, 1), Y=(64, 1, 1))], Ls=0)
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"]),
+              W.SubSweep(W.DS, b=[1], dims=[(e["p1"], e["p2"], 1, 1)], Ls=[0]))
+    assert pr.t_ge == e["expect"]
+    r = EX["reduce_to_leader"]
+    pr1 = _one(oracle_mod, toys.model([toys.row(w=r["m"], X=(64, 1, 1))], Ls=0),
+               toys.system(alpha=r["alpha"], beta=r["beta"]),
+               W.SubSweep(W.DS, b=[1], dims=[(1, r["p"], 1, 1)], Ls=[0]))
+    assert pr1.t_ge == r["expect"]
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8, 13])
+@pytest.mark.parametrize("mbytes", [1, 8, 1000, 123457])
+def test_allreduce_matches_ring_simulation(oracle_mod, p, mbytes):
+    a, b = 3e-6, 1.0 / 7e9
+    t_sim, acc = brute.ring_allreduce_sim(p, mbytes, Fr(a), Fr(b))
+    col = [sum((i + 1) * 1000 + c for i in range(p)) for c in range(p)]
+    assert all(row == col for row in acc)          # the simulated ring really reduces
+    pr = _one(oracle_mod, toys.model([toys.row(w=mbytes)]), toys.system(alpha=a, beta=b),
+              W.SubSweep(W.DATA, b=[1], dims=[(p, 1, 1, 1)]))
+    assert _rel(pr.t_ge, t_sim) <= 4e-16
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 7, 16])
+def test_allgather_matches_ring_simulation(oracle_mod, p):
+    a, b = 2e-6, 1.0 / 3e9
+    y = 777 * p
+    t_sim = brute.ring_allgather_sim(p, Fr(y, p), Fr(a), Fr(b))
+    m = toys.model([toys.row(y=y, F=64), toys.row(F=64)])
+    pr = _one(oracle_mod, m, toys.system(alpha=a, beta=b), W.SubSweep(W.FILTER, b=[1], dims=[(p, 1, 1, 1)]))
+    assert _rel(pr.t_fb_ag, t_sim) <= 4e-16
+
+
+def test_no_comm_at_p1_and_monotone(oracle_mod):
+    # north_star invariants: no communication term at p = 1; costs monotone in message size
+    base = toys.system(alpha=1e-5, beta=1e-9)
+    for fam in (W.DATA, W.FILTER, W.CHANNEL, W.SPATIAL):
+        m = toys.model([toys.row(w=100, y=50, X=(8, 8, 1), Y=(8, 8, 1), K=(3, 3, 1), C=4, F=4)])
+        pr = _one(oracle_mod, m, base, W.SubSweep(fam, b=[2], dims=[(1, 1, 1, 1)], Ls=[1]))
+        assert pr.t_ge == pr.t_fb_ag == pr.t_fb_ar == pr.t_halo == pr.t_p2p == 0.0
+    prev = -1.0
+    for w in [1, 10, 1000, 10 ** 6, 10 ** 9]:
+        pr = _one(oracle_mod, toys.model([toys.row(w=w)]), base, W.SubSweep(W.DATA, b=[1], dims=[(8, 1, 1, 1)]))
+        assert pr.t_ge > prev
+        prev = pr.t_ge
+
+
+def test_allreduce_bandwidth_asymptote(oracle_mod):
+    # S:203 / north_star: AR(p,m)/m -> 2(p-1)/p beta; at m = 1 GB within 1%
+    beta = 1e-10
+    for p in (2, 8, 64, 1024):
+        pr = _one(oracle_mod, toys.model([toys.row(w=10 ** 9)]), toys.system(alpha=1e-7, beta=beta),
+                  W.SubSweep(W.DATA, b=[1], dims=[(p, 1, 1, 1)]))
+        ratio = pr.t_ge / 1e9
+        assert abs(ratio / (2 * (p - 1) / p * beta) - 1) < 0.01
+
+
+def test_contention_phi_doubles_beta_part(oracle_mod):
+    # doubling phi doubles only the beta contribution (df inter-group GE)
+    m = toys.model([toys.row(w=4096, y=8, F=64), toys.row(F=64)])
+    ge = {}
+    for phi in (1.0, 2.0):
+        for a in (0.0, 1e-5):
+            pr = _one(oracle_mod, m, toys.system(alpha=a, beta=1e-9, phi=phi),
+                      W.SubSweep(W.DF, b=[1], dims=[(4, 2, 1, 1)]))
+            ge[(phi, a)] = pr.t_ge
+    beta1 = ge[(1.0, 0.0)]
+    assert ge[(2.0, 0.0)] == 2 * beta1
+    assert _rel(ge[(2.0, 1e-5)] - ge[(1.0, 1e-5)], beta1) < 1e-12
+
+
+def test_weak_scaling_ge_ratio(oracle_mod):
+    e = EX["weak_scaling_ratio"]
+    m = toys.model([toys.row(w=10 ** 8, fw=10, bw=20, wu=7)], D=10 ** 6)
+    out = {}
+    for p in (e["p_lo"], e["p_hi"]):
+        out[p] = _one(oracle_mod, m, toys.system(alpha=0.0, beta=1e-9),
+                      W.SubSweep(W.DATA, b=[4], dims=[(p, 1, 1, 1)]))
+    assert abs(out[e["p_hi"]].t_ge / out[e["p_lo"]].t_ge / e["expect"] - 1) <= 1e-12
+    # weak scaling: per-PE compute independent of p when B = b p
+    assert out[e["p_hi"]].t_comp == out[e["p_lo"]].t_comp
+
+
+# ------------------------------------------------------------ Table 2 rows: worked examples
+def test_serial_examples(oracle_mod):
+    e = EX["serial_comp_epoch"]
+    m = toys.model([toys.row(fw=e["FW"], bw=e["BW"], wu=e["WU"])], D=e["D"])
+    pr = _one(oracle_mod, m, toys.system(R=1.0), W.SubSweep(W.SERIAL, b=[e["B"]]))
+    assert pr.t_comp * pr.I == e["expect"]
+    e = EX["serial_mem"]
+    m = toys.model([toys.row(x=e["x"], y=e["y"], w=e["w"], bi=e["bi"])])
+    pr = _one(oracle_mod, m, toys.system(delta=e["delta"], gamma=e["gamma"]), W.SubSweep(W.SERIAL, b=[e["B"]]))
+    assert pr.mem == e["expect"]
+
+
+def test_data_comp_example(oracle_mod):
+    e = EX["data_comp_epoch"]
+    m = toys.model([toys.row(fw=e["FW"], bw=e["BW"], wu=e["WU"])], D=e["D"])
+    pr = _one(oracle_mod, m, toys.system(R=1.0), W.SubSweep(W.DATA, b=[e["B"] // e["p"]], dims=[(e["p"], 1, 1, 1)]))
+    assert pr.B == e["B"]
+    assert pr.t_comp * pr.I == e["expect"]
+
+
+def test_halo_elements_examples(oracle_mod):
+    e = EX["halo_elements"]
+    r = M.make_conv("c", e["C"], e["C"], tuple(e["X"]), e["K"], stride=1, pad=1)
+    for pw, expect in e["cases"]:
+        assert oracle_mod.halo_elements(r, (pw, 1, 1), 0) == expect
+        assert oracle_mod.halo_elements(r, (pw, 1, 1), 1) == expect
+    r1 = M.make_conv("c1", 3, 3, (226, 226), 1)
+    assert oracle_mod.halo_elements(r1, (4, 4, 1), 0) == 0          # K = 1: no halo
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_halo_matches_remote_index_enumeration(oracle_mod, seed):
+    """Brute force: count remote input cells a PE needs (faces only, Q15) on small grids."""
+    rng = random.Random(seed)
+    nd = rng.choice([1, 2, 3])
+    X = tuple(rng.randint(4, 12) for _ in range(nd))
+    K = rng.choice([3, 5])
+    C = rng.randint(1, 3)
+    r = M.make_conv("c", C, C, X, K, stride=1, pad=K // 2)
+    split = [1, 1, 1]
+    ax = rng.randrange(nd)
+    split[ax] = rng.choice([2, 3, 4])
+    # interior PE along `ax` (or PE 0 if 2 parts): enumerate cells within K//2 outside its slab
+    h = K // 2
+    n = X[ax]
+    loc = -(-n // split[ax])
+    part = 1 if split[ax] > 2 else 0
+    lo, hi = part * loc, min(n, (part + 1) * loc)
+    cells = 0
+    for cidx in itertools.product(*[range(v) for v in X]):
+        c = cidx[ax]
+        if (lo - h <= c < lo) or (hi <= c < hi + h):
+            cells += 1
+    expect = C * cells
+    if split[ax] > 2 and hi + h > n:
+        pytest.skip("interior slab touches the boundary (ragged split)")
+    if loc < h:
+        pytest.skip("SplitTooFine: the halo would span several PEs (infeasible)")
+    got =oracle_mod.halo_elements(r, tuple(split), 0)
+    assert got == expect
+
+
+def test_spatial_halo_iteration_example(oracle_mod):
+    e = EX["spatial_halo_iter"]
+    r = M.make_conv("c", 3, 3, (226, 226), 3, stride=1, pad=1)
+    r.flags |= M.FLAG_FOLDED
+    m = toys.model([r], Ls=1)
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"], delta=e["delta"]),
+              W.SubSweep(W.SPATIAL, b=[e["B"]], dims=[(1, 2, 1, 1)], Ls=[1]))
+    assert abs(pr.t_halo - e["expect"]) <= 1e-18
+
+
+def test_layer_pure_example(oracle_mod):
+    e = EX["layer_pure_p2p_iter"]
+    m = toys.model([toys.row(y=e["y"]), toys.row(y=1)])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"], delta=e["delta"]),
+              W.SubSweep(W.LAYERPURE, b=[e["B"]], part_mode=W.PART_COMB, s_min=2, s_max=2))
+    assert pr.t_p2p == e["expect"]
+
+
+def test_pipeline_examples(oracle_mod):
+    e = EX["pipeline_comp_epoch"]
+    m = toys.model([toys.row(fw=1, bw=1), toys.row(fw=1, bw=1)], D=e["D"])
+    pr = _one(oracle_mod, m, toys.system(R=1.0),
+              W.SubSweep(W.PIPELINE, b=[e["B"]], S=[e["S"]], part_mode=W.PART_COMB, s_min=2, s_max=2))
+    assert pr.t_comp * pr.I == e["expect"]
+    e = EX["pipeline_comm_iter"]
+    m = toys.model([toys.row(y=e["y"]), toys.row(y=3)])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"], delta=e["delta"]),
+              W.SubSweep(W.PIPELINE, b=[e["B"]], S=[e["S"]], part_mode=W.PART_COMB, s_min=2, s_max=2))
+    assert pr.t_p2p == e["expect"]
+
+
+def test_partition_balanced_example(oracle_mod):
+    e = EX["partition_balanced"]
+    m = toys.model([toys.row(fw=c, bw=0) for c in e["costs"]], D=1)
+    sw = toys.sweep(m, toys.system(R=1.0), [W.SubSweep(W.PIPELINE, b=[1], S=[1], part_mode=W.PART_COMB,
+                                                        s_min=e["p"], s_max=e["p"])])
+    o = oracle_mod.OracleSweep(sw)
+    (best, key), = o.topk(0, o.size(), 1)[0][:1]
+    # comp = (s+S-1)(B/S) maxFW = 2 * bottleneck  ->  bottleneck 4 with the cut after row 2
+    assert key == 2 * e["bottleneck"]
+    assert list(o.decode(best).stage_end[:2]) == [2, 4]
+
+
+def test_filter_and_df_examples(oracle_mod):
+    e = EX["filter_comm_epoch"]
+    m = toys.model([toys.row(y=e["y1"], F=64), toys.row(F=64)], D=e["B"])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"], delta=e["delta"]),
+              W.SubSweep(W.FILTER, b=[e["B"]], dims=[(e["p"], 1, 1, 1)]))
+    assert (pr.t_fb_ag + pr.t_fb_ar) * pr.I == e["expect"]
+    e = EX["df_comm_epoch"]
+    m = toys.model([toys.row(y=e["y1"], F=64, w=e["W"]), toys.row(F=64)], D=e["B"])
+    pr = _one(oracle_mod, m, toys.system(alpha=e["alpha"], beta=e["beta"], delta=e["delta"], phi=1.0),
+              W.SubSweep(W.DF, b=[e["B"] // e["p1"]], dims=[(e["p1"], e["p2"], 1, 1)]))
+    assert (pr.t_fb_ag + pr.t_fb_ar + pr.t_ge) * pr.I == e["expect"]
+
+
+def test_gpipe_schedule_vs_closed_form(oracle_mod):
+    """Equal groups: the discrete-event makespan equals (p+S-1)(B/S)(FW+BW).
+    Unequal groups: the closed form uses the slowest stage, so it upper-bounds the
+    schedule, which is itself at least S segments of the slowest stage (Q34)."""
+    rng = random.Random(3)
+    for trial in range(200):
+        s = rng.choice([2, 3, 4])
+        S = rng.choice([1, 2, 4, 8])
+        B = S * rng.choice([1, 2, 3])
+        equal = trial < 40
+        f = [rng.randint(1, 9) for _ in range(s)]
+        g = [rng.randint(1, 9) for _ in range(s)]
+        if equal:
+            f = [f[0]] * s
+            g = [g[0]] * s
+        rows = [toys.row(fw=f[i], bw=g[i]) for i in range(s)]
+        m = toys.model(rows, D=B)
+        pr = _one(oracle_mod, m, toys.system(R=1.0),
+                  W.SubSweep(W.PIPELINE, b=[B], S=[S], part_mode=W.PART_COMB, s_min=s, s_max=s))
+        des = brute.gpipe_makespan([Fr(v) for v in f], [Fr(v) for v in g], S, Fr(B, S))
+        if equal:
+            assert Fr(pr.t_comp) == des
+        else:
+            assert des <= Fr(pr.t_comp)
+            assert des >= S * Fr(B, S) * (max(f) + max(g)) / 2
+
+
+# ------------------------------------------------------------ memory
+@pytest.mark.parametrize("seed", range(25))
+def test_memory_rows_equal_buffer_enumeration(oracle_mod, seed):
+    sw = corpus.random_sweep(seed)
+    o = oracle_mod.OracleSweep(sw)
+    n = o.size()
+    rng = random.Random(seed)
+    confs = list(brute.enumerate_configs(sw))
+    for idx, cfg in rng.sample(confs, min(60, len(confs))):
+        pr = o.explain(idx)
+        want = brute.buffer_bytes(sw, cfg)
+        assert _rel(pr.mem, want) <= 1e-15, (idx, cfg["family"])
+    assert n == len(confs)
+
+
+# ------------------------------------------------------------ exact rational evaluator
+@pytest.mark.parametrize("seed", range(30))
+def test_oracle_matches_exact_rationals(oracle_mod, seed):
+    sw = corpus.random_sweep(seed)
+    o = oracle_mod.OracleSweep(sw)
+    confs = list(brute.enumerate_configs(sw))
+    rng = random.Random(1000 + seed)
+    for idx, cfg in rng.sample(confs, min(80, len(confs))):
+        pr = o.explain(idx)
+        ex = brute.exact(sw, cfg)
+        assert pr.reason == ex["reason"], (idx, cfg, pr.reason, ex["reason"])
+        assert pr.B == ex["B"] and pr.p == ex["p"]
+        for f in ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_halo", "t_p2p", "t_iter", "mem", "I"):
+            v = ex[f]
+            got = getattr(pr, f)
+            if v is None:
+                assert math.isinf(got), (f, idx)
+            else:
+                assert _rel(got, v) <= 1e-14, (f, idx, cfg["family"], got, float(v))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_decoder_matches_itertools_enumeration(oracle_mod, seed):
+    sw = corpus.random_sweep(seed, max_list=2)
+    o = oracle_mod.OracleSweep(sw)
+    confs = list(brute.enumerate_configs(sw))
+    assert o.size() == len(confs)
+    rng = random.Random(seed)
+    for idx, cfg in rng.sample(confs, min(300, len(confs))):
+        c = o.decode(idx)
+        assert c.sub == cfg["sub"] and c.b == cfg["b"] and c.S == cfg["S"]
+        assert tuple(c.dims) == tuple(cfg["dims"]) and c.Ls == cfg["Ls"]
+        assert tuple(c.stage_end[:c.n_stages]) == cfg["ends"]
+        nt = len(sw.system.tiers)
+        assert list(c.alpha[:nt]) == list(cfg["alpha"]) and list(c.beta[:nt]) == list(cfg["beta"])
+        assert c.cap == cfg["cap"] and c.flops == cfg["R"]
+
+
+def test_partition_counts():
+    from math import comb
+    for G in range(1, 20):
+        assert sum(comb(G - 1, s - 1) for s in range(1, G + 1)) == 2 ** (G - 1)
+    assert sum(comb(151, k) for k in range(6)) == 633_245_832
+    assert sum(comb(49, k) for k in range(4)) == 19650
+
+
+# ------------------------------------------------------------ literal fold vs canonical trees
+@pytest.mark.parametrize("seed", range(30))
+def test_canonical_tree_matches_literal_fold(oracle_mod, seed):
+    sw = corpus.random_sweep(seed)
+    o = oracle_mod.OracleSweep(sw)
+    n = o.size()
+    rng = random.Random(seed)
+    for idx in rng.sample(range(n), min(200, n)):
+        a = o.explain(idx)
+        b = o.explain(idx, fold=True)
+        for f in ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_halo", "t_p2p", "t_iter", "mem"):
+            x, y = getattr(a, f), getattr(b, f)
+            if math.isinf(x) or math.isinf(y):
+                assert x == y
+            else:
+                assert _rel(x, y) <= 1e-12, (f, idx, x, y)
+
+
+# ------------------------------------------------------------ degenerate identities (tolerance 0)
+def _pred(o, sub_i, sw, **fix):
+    confs = [c for c in brute.enumerate_configs(sw) if c[1]["sub"] == sub_i]
+    for idx, cfg in confs:
+        if all(cfg[k] == v for k, v in fix.items()):
+            return o.explain(idx)
+    raise KeyError(fix)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_degenerate_identities(oracle_mod, seed):
+    m = corpus.random_model(seed)
+    sysd = corpus.random_system(seed)
+    nt = len(sysd.tiers)
+    A = [[1e-5 * (t + 1) for t in range(nt)]]
+    Bt = [[1e-9 * (t + 1) for t in range(nt)]]
+    b = 4
+    P = [2, 3, 4]
+    subs = [
+        W.SubSweep(W.SERIAL, b=[b], alpha=A, beta=Bt),                                           # 0
+        W.SubSweep(W.DATA, b=[b], dims=[(1, 1, 1, 1)] + [(p, 1, 1, 1) for p in P], alpha=A, beta=Bt),
+        W.SubSweep(W.SPATIAL, b=[b], dims=[(1, 1, 1, 1), (1, 2, 1, 1), (1, 2, 2, 1)], Ls=[m.G], alpha=A, beta=Bt),
+        W.SubSweep(W.FILTER, b=[b], dims=[(1, 1, 1, 1)] + [(p, 1, 1, 1) for p in P], alpha=A, beta=Bt),
+        W.SubSweep(W.CHANNEL, b=[b], dims=[(1, 1, 1, 1)] + [(p, 1, 1, 1) for p in P], alpha=A, beta=Bt),
+        W.SubSweep(W.DF, b=[b], dims=[(1, p, 1, 1) for p in P] + [(p, 1, 1, 1) for p in P], alpha=A, beta=Bt),
+        W.SubSweep(W.DS, b=[b], dims=[(p, 1, 1, 1) for p in P] + [(1, 2, 1, 1), (1, 2, 2, 1)], Ls=[m.G],
+                   alpha=A, beta=Bt),
+        W.SubSweep(W.PIPELINE, b=[b], S=[1, 2], part_mode=W.PART_COMB, s_min=1, s_max=min(3, m.G), alpha=A, beta=Bt),
+        W.SubSweep(W.PD, b=[b], S=[1, 2], dims=[(1, 1, 1, 1)], part_mode=W.PART_COMB, s_min=1,
+                   s_max=min(3, m.G), alpha=A, beta=Bt),
+    ]
+    sw = W.Sweep([m], sysd, subs, "deg")
+    o = oracle_mod.OracleSweep(sw)
+    fields = ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_halo", "t_p2p", "t_iter", "t_epoch", "mem", "reason")
+
+    def same(x, y, fs=fields):
+        for f in fs:
+            assert getattr(x, f) == getattr(y, f), f
+
+    serial = _pred(o, 0, sw)
+    for si, d in ((1, (1, 1, 1, 1)), (2, (1, 1, 1, 1)), (3, (1, 1, 1, 1)), (4, (1, 1, 1, 1))):
+        x = _pred(o, si, sw, dims=d)
+        same(x, serial, ("t_comp", "t_iter", "t_epoch", "mem"))
+    for p in P:
+        f = _pred(o, 3, sw, dims=(p, 1, 1, 1))
+        c = _pred(o, 4, sw, dims=(p, 1, 1, 1))
+        same(f, c, ("t_comp", "t_iter", "t_epoch", "mem"))                  # filter == channel
+        same(_pred(o, 5, sw, dims=(1, p, 1, 1)), f, fields[:-1])            # df(1,p) == filter(p)
+        same(_pred(o, 5, sw, dims=(p, 1, 1, 1)), _pred(o, 1, sw, dims=(p, 1, 1, 1)))   # df(p,1) == data(p)
+        same(_pred(o, 6, sw, dims=(p, 1, 1, 1)), _pred(o, 1, sw, dims=(p, 1, 1, 1)))   # ds(p;1) == data(p)
+    for d in ((1, 2, 1, 1), (1, 2, 2, 1)):
+        same(_pred(o, 6, sw, dims=d), _pred(o, 2, sw, dims=d))                     # ds(1;split) == spatial
+    pipe1 = _pred(o, 7, sw, ends=(m.G,), S=1)
+    assert pipe1.t_comp == serial.t_comp                                           # pipeline(1,1) == serial comp
+    for c in brute.enumerate_configs(sw):
+        if c[1]["sub"] == 8:
+            q = _pred(o, 7, sw, ends=c[1]["ends"], S=c[1]["S"])
+            same(o.explain(c[0]), q)                                               # pd(1) == pipeline
+
+
+# ------------------------------------------------------------ paper pins: layer tables, limits
+def test_table4_layer_tables():
+    pin = PIN["table4_layers"]
+    assert M.resnet(50).G == pin["resnet50"]
+    assert M.resnet(152).G == pin["resnet152"]
+    assert M.vgg16().G == pin["vgg16"]
+    assert M.cosmoflow(256).G == pin["cosmoflow"]
+    pp = PIN["table4_params_approx"]
+    for name, mdl in (("resnet50", M.resnet(50)), ("resnet152", M.resnet(152)),
+                      ("vgg16", M.vgg16()), ("cosmoflow", M.cosmoflow(256))):
+        tol = pp["vgg16_rel_tol"] if name == "vgg16" else pp["rel_tol"]
+        assert abs(M.param_count(mdl) / pp[name] - 1) <= tol, name
+    assert M.resnet(50).D == 1_281_167 and abs(M.resnet(50).D / PIN["imagenet_samples"]["D_approx"] - 1) < 0.01
+    assert M.cosmoflow(512).D == PIN["cosmoflow_samples"]["D"]
+    assert M.vgg16().layers[0].C == PIN["channel_first_layer"]["first_C"]
+    c1 = M.cosmoflow(512).layers[0]
+    assert (c1.x + c1.y) * PIN["cosmoflow512_conv1_activation"]["delta"] > PIN["cosmoflow512_conv1_activation"]["min_bytes"]
+
+
+def test_filter_limit_64(oracle_mod):
+    pin = PIN["filter_limit"]
+    for name in ("vgg16", "resnet50"):
+        m = M.by_name(name)
+        sw = W.Sweep([m], W.two_tier_system(hbm_bytes=1e30),
+                     [W.SubSweep(W.FILTER, b=[1], dims=[(pin[name], 1, 1, 1), (2 * pin[name], 1, 1, 1)])])
+        o = oracle_mod.OracleSweep(sw)
+        assert o.explain(0).reason & brute.R_SCALING == 0
+        assert o.explain(1).reason & brute.R_SCALING
+
+
+def test_cosmoflow_data_parallel_memory_infeasible(oracle_mod):
+    """CosmoFlow 512^3 cannot run data-parallel in 16 GB; ds with a spatial split can
+    (SPEC acceptance 10).  The rejection reason is Memory, not ScalingLimit."""
+    m = M.cosmoflow(512)
+    cap = PIN["cosmoflow_data_infeasible"]["cap_bytes"]
+    sysd = W.two_tier_system(hbm_bytes=cap)
+    sw = W.Sweep([m], sysd, [
+        W.SubSweep(W.DATA, b=[1], dims=[(p, 1, 1, 1) for p in (1, 16, 256)]),
+        W.SubSweep(W.FILTER, b=[1], dims=[(4, 1, 1, 1)]),
+        W.SubSweep(W.PIPELINE, b=[1], part_mode=W.PART_COMB, s_min=1, s_max=4),
+        W.SubSweep(W.DS, b=[1], dims=[(4, 4, 4, 2)], Ls=[6]),
+    ])
+    o = oracle_mod.OracleSweep(sw)
+    for i in range(3):
+        r = o.explain(i).reason
+        assert r & brute.R_MEMORY and not r & brute.R_SCALING
+    assert o.explain(3).reason & brute.R_MEMORY
+    npipe = 1 + 19 + 171 + 969
+    assert all(o.explain(4 + i).reason & brute.R_MEMORY for i in range(npipe))
+    assert o.explain(4 + npipe).feasible
+
+
+def test_config1_expectations(oracle_mod):
+    """22 of 33 feasible; argmin p=1024, b=64 (idx 31); b=128 needs > 16 GiB."""
+    sw = W.config1()
+    o = oracle_mod.OracleSweep(sw)
+    hits, nf = o.topk(0, o.size(), 3)
+    assert o.size() == 33 and nf == 22
+    assert hits[0][0] == 31
+    c = o.decode(31)
+    assert c.b == 64 and c.dims[0] == 1024
+    for idx in range(33):
+        pr = o.explain(idx)
+        assert (pr.reason == 0) == (o.decode(idx).b != 128)
