@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""bench.py -- configurations evaluated per second by the ParaDL sweep on 1..8 B200.
+
+Workload (BASELINE.json configs[1]): ResNet-50, six strategies
+(data, spatial, filter, channel, data+filter, data+spatial, pipeline s<=4) x b in 2^0..2^8
+x a 64x64 alpha/beta grid = 2,914,136,064 configurations per step.  A step is one pass of
+the hot path over the whole sweep: decode -> Table 2 cost -> feasibility -> top-64 /
+argmin / feasible count, per rank over its tile shard, then (N > 1) one NCCL all_gather
+of the per-rank top-k and the device merge.  `value` = configurations / s for the whole
+job (inputs resident: model + spec image loaded before the timed region); `e2e` = the
+same through the public C-ABI with host inputs and host results (paradl_set_system +
+paradl_topk each step, which re-uploads the spec image and reads back the hits).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+Under torchrun (N > 1) each rank drives LOCAL_RANK's GPU; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_TOP = 64
+# FP64-pipe instructions per configuration in the inner (alpha/beta) loop of the
+# dominant kernel, counted from the canonical tree: pipeline family:
+# s*beta, alpha+, c*, comp+, *I, compare  = 6
+FP64_OPS_PER_CONFIG = {"pipeline": 6, "data": 6, "filter": 9, "channel": 9, "spatial": 11, "df": 14,
+                       "ds": 15, "pd": 10, "layerpure": 7, "serial": 3}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks (nvidia-smi)
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names[1:], parts[5:9]):
+                if v.lower() in ("active", "0x1", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_baseline(sweep, target_s: float, rank: int = 0):
+    """The oracle as it stands, on all host cores, on a bounded sample of the same sweep:
+    contiguous windows of 4096 configurations at evenly spaced offsets."""
+    from oracle import oracle as O
+    osw = O.OracleSweep(sweep)
+    n = osw.size()
+    cores = os.cpu_count() or 1
+
+    def run(nwin):
+        stride = n // nwin
+        t0 = time.perf_counter()
+        tot = 0
+        for w in range(nwin):
+            a = w * stride
+            c = min(4096, n - a)
+            osw.topk(a, c, K_TOP, nthreads=cores)
+            tot += c
+        return tot, time.perf_counter() - t0
+
+    tot, dt = run(8)
+    nwin = max(8, int(8 * target_s / max(dt, 1e-3)))
+    tot, dt = run(nwin)
+    return {"value": tot / dt, "unit": "configs/s", "cores": cores, "kind": "oracle",
+            "sample": f"{nwin} windows x 4096 consecutive configs evenly spaced over the {n}-config sweep "
+                      f"({tot} configs, {dt:.1f} s, top-{K_TOP} + count per window)"}
+
+
+def reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from workloads import sweeps as W
+    sweep = W.CONFIGS[args.config]()
+    base = {"metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
+            "unit": "configs/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": sweep.name}}
+    per_step_s = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    from oracle import oracle as O
+    osw = O.OracleSweep(sweep)
+    n = osw.size()
+    cores = os.cpu_count() or 1
+    # calibrate windows per step so one step takes about per_step_s seconds
+    t0 = time.perf_counter()
+    osw.topk(0, 4096, K_TOP, nthreads=cores)
+    dt1 = time.perf_counter() - t0
+    nwin = max(1, int(per_step_s / max(dt1, 1e-4)))
+    stride = max(1, n // nwin)
+    times = []
+    tot = 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for w in range(nwin):
+            a = (w * stride + s * 4096) % max(1, n - 4096)
+            osw.topk(a, 4096, K_TOP, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            tot += nwin * 4096
+    v = tot / sum(times)
+    line = dict(base, value=v, ms_per_step=1e3 * sum(times) / len(times),
+                cpu_baseline={"value": v, "unit": "configs/s", "cores": cores, "kind": "oracle",
+                              "sample": f"per step {nwin} windows x 4096 consecutive configs spread over the sweep"},
+                e2e={"value": v, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                vs_baseline=None, scaling="weak")
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    n_gpus = ws
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_2104_09075_b200 as P
+    from workloads import sweeps as W
+
+    sweep = W.CONFIGS[args.config]()
+    ctx = P.Context(dev.index)
+    spec = ctx.prepare(sweep)
+    N = ctx.sweep_size(spec)
+    stream = torch.cuda.current_stream()
+
+    lists = torch.empty((max(ws, 1), K_TOP, 2), dtype=torch.int64, device=dev)
+    counts = torch.zeros(max(ws, 1), dtype=torch.int64, device=dev)
+    my_hits = torch.empty((K_TOP, 2), dtype=torch.int64, device=dev)
+    my_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    out = torch.empty((K_TOP, 2), dtype=torch.int64, device=dev)
+    out_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    launches = [0]
+
+    def step():
+        ctx.topk_async(spec, 0, N, rank, ws, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        launches[0] += ctx.stat(2)
+        if ws > 1:
+            dist.all_gather_into_tensor(lists.view(ws, -1), my_hits.view(-1))
+            dist.all_gather_into_tensor(counts, my_cnt)
+            ctx.merge_topk(lists.data_ptr(), ws, K_TOP, counts.data_ptr(), out.data_ptr(), out_cnt.data_ptr(),
+                           stream=stream)
+            launches[0] += 1
+            return out, out_cnt
+        return my_hits, my_cnt
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    sampler = ClockSampler(dev.index if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    sampler.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches[0] = 0
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)              # L2 flush between timed steps (not timed)
+        evs[i][0].record(stream)
+        res, rc = step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    value = N * args.steps / (t_ms * 1e-3)
+    gpu_launches = launches[0]
+    best = res.cpu().numpy()
+    n_feasible = int(rc.item())
+
+    # ---- e2e: public C-ABI, host inputs (spec image re-uploaded) and host results
+    e2e_ms = []
+    h2d = d2h = 0
+    if ws == 1:
+        for i in range(args.warmup + args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            ctx.set_system(sweep.system)          # invalidates the resident image -> H2D each step
+            hits, nf = ctx.topk(spec, K_TOP, 0, N, stream=stream)
+            h2d, d2h = ctx.stat(0), ctx.stat(1)
+            t1.record(stream)
+            t1.synchronize()
+            if i >= args.warmup:
+                e2e_ms.append(t0.elapsed_time(t1))
+        assert nf == n_feasible and hits[0][0] == int(best[0, 0]) % (1 << 64)
+    else:
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            ctx.set_system(sweep.system)
+            ctx.topk_async(spec, 0, N, rank, ws, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+            h2d = ctx.stat(0)
+            dist.all_gather_into_tensor(lists.view(ws, -1), my_hits.view(-1))
+            dist.all_gather_into_tensor(counts, my_cnt)
+            ctx.merge_topk(lists.data_ptr(), ws, K_TOP, counts.data_ptr(), out.data_ptr(), out_cnt.data_ptr(),
+                           stream=stream)
+            host = out.cpu()
+            _ = out_cnt.cpu()
+            d2h = host.numel() * 8 + 8
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if i >= args.warmup:
+                e2e_ms.append(float(dt.item()) * 1e3)
+    e2e_value = N * len(e2e_ms) / (sum(e2e_ms) * 1e-3)
+
+    # ---- roofline of the dominant kernel (pipeline family: 78,600 of 79,051 configs per outer tuple)
+    roof = None
+    fp64_peak = ctx.fp64_peak(60.0)
+    dom = [i for i, s in enumerate(sweep.subs) if s.family == W.PIPELINE]
+    if dom:
+        sub = sweep.subs[dom[0]]
+        dspec = P.Spec([sub], [spec_model_id(ctx, spec, dom[0])])
+        ctx.set_system(sweep.system)
+        nd = ctx.sweep_size(dspec)
+        for _ in range(3):
+            ctx.topk_async(dspec, 0, nd, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        kev = []
+        for i in range(10):
+            flush.fill_(2)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            ctx.topk_async(dspec, 0, nd, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+            b_.record(stream)
+            kev.append((a_, b_))
+        torch.cuda.synchronize()
+        kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+        ops = nd * FP64_OPS_PER_CONFIG["pipeline"]
+        achieved = ops / (kms * 1e-3) / 1e12
+        peak = fp64_peak / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("sweep_kernel_pipeline_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T fp64-pipe inst/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "sweep_kernel<PIPELINE,reduce> (+merge)", "configs_per_launch": nd,
+                "fp64_inst_per_config": FP64_OPS_PER_CONFIG["pipeline"], "launch_ms": kms,
+                "peak_source": "measured DFMA-chain microbenchmark (paradl_fp64_peak) in this run",
+                "peak_nominal_T": 148 * 64 * 1.965e9 / 1e12,
+                "frac_of_nominal": achieved / (148 * 64 * 1.965e9 / 1e12),
+                "configs_per_s": nd / (kms * 1e-3)}
+        ctx.set_system(sweep.system)
+
+    # ---- dense mode (a9): HBM-write-bound secondary figure
+    dense = None
+    if not args.no_dense and ws == 1:
+        cnt = 1 << 28
+        t = torch.empty(cnt, dtype=torch.float64, device=dev)
+        m = torch.empty(cnt, dtype=torch.float64, device=dev)
+        bits = torch.empty(cnt // 32, dtype=torch.int32, device=dev)
+        rs = torch.empty(cnt, dtype=torch.uint8, device=dev)
+        first = N // 3
+        for _ in range(2):
+            ctx.sweep_dense(spec, first, cnt, t.data_ptr(), m.data_ptr(), bits.data_ptr(), rs.data_ptr(), stream=stream)
+        dv = []
+        for _ in range(5):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            ctx.sweep_dense(spec, first, cnt, t.data_ptr(), m.data_ptr(), bits.data_ptr(), rs.data_ptr(), stream=stream)
+            b_.record(stream)
+            dv.append((a_, b_))
+        torch.cuda.synchronize()
+        dms = statistics.mean(a.elapsed_time(b) for a, b in dv)
+        nbytes = cnt * (8 + 8 + 1) + cnt // 8
+        dense = {"configs": cnt, "ms": dms, "configs_per_s": cnt / (dms * 1e-3),
+                 "write_GBps": nbytes / (dms * 1e-3) / 1e9, "hbm_peak_GBps": 6538.3,
+                 "frac": nbytes / (dms * 1e-3) / 1e9 / 6538.3, "bytes_per_config": 17.125}
+        del t, m, bits, rs
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(sweep, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
+            "value": value, "unit": "configs/s", "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": sweep.name, "configs_per_step": N, "k": K_TOP,
+                       "model": "resnet50 layer table (Table 4 shape, synthetic FLOP parametrisation)",
+                       "parallelism": f"index-range shards x{ws} + NCCL all_gather merge",
+                       "l2": "flushed (256 MiB device write) before every timed step; inputs are a KB-size image"},
+            "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(gpu_launches),
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "dense": dense,
+            "result": {"argmin_idx": int(best[0, 0]) % (1 << 64), "n_feasible": n_feasible},
+            "fp64_peak_inst_per_s": fp64_peak,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def spec_model_id(ctx, spec, sub_index):
+    return spec.c.sub[sub_index].model_id
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,777 @@
+// api.cpp -- host side of libparadl: the C ABI of include/paradl.h.
+//
+// Responsibilities: input validation and overflow proofs, the canonical
+// index space of a sweep (mixed radices, partition counts), packing the device image that
+// the kernels stage into shared memory, launch configuration (persistent grid sized from
+// the occupancy API and the SM count), and result transfer.  No cost-model arithmetic is
+// done here: every Table 2 term is evaluated by the kernels in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "paradl_internal.h"
+
+using namespace paradl;
+
+namespace {
+
+struct HostModel {
+    std::vector<paradl_layer> rows;
+    int64_t D = 0;
+    ModelHdr layout{};
+    uint8_t *d_block = nullptr;
+    // host-side bounds for overflow proofs only
+    __int128 FB = 0, XY = 0, W = 0, BI = 0, Ysum = 0, Ymax = 0, Hmax = 0;
+};
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) n = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+}  // namespace
+
+struct paradl_ctx {
+    int device = -1;
+    int n_sm = 0;
+    size_t smem_optin = 0;
+    std::string err;
+    bool have_system = false;
+    paradl_system sys{};
+    std::vector<HostModel> models;
+    // device scratch
+    DevBuf img, lists, counters, results, one;
+    std::vector<uint8_t> last_img;     // host copy of the image currently on the device
+    uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
+    uint64_t models_epoch = 0, img_epoch = ~0ull;
+};
+
+static paradl_status fail(paradl_ctx *c, paradl_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                          \
+    do {                                                                                             \
+        cudaError_t e_ = (expr);                                                                     \
+        if (e_ != cudaSuccess) return fail(ctx, PARADL_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+static const __int128 kLimit = (__int128)1 << 62;
+
+// ------------------------------------------------------------------ lifecycle
+extern "C" paradl_status paradl_create(int32_t cuda_device, paradl_ctx **out) {
+    if (!out) return PARADL_EINVAL;
+    *out = nullptr;
+    paradl_ctx *c = new (std::nothrow) paradl_ctx();
+    if (!c) return PARADL_ENOMEM;
+    c->device = cuda_device;
+    if (cuda_device >= 0) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device >= n) {
+            delete c;
+            return PARADL_ECUDA;
+        }
+        if (cudaSetDevice(cuda_device) != cudaSuccess) {
+            delete c;
+            return PARADL_ECUDA;
+        }
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, cuda_device);
+        c->n_sm = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, cuda_device);
+        c->smem_optin = (size_t)v;
+    }
+    *out = c;
+    return PARADL_OK;
+}
+
+extern "C" void paradl_destroy(paradl_ctx *c) {
+    if (!c) return;
+    if (c->device >= 0) {
+        cudaSetDevice(c->device);
+        for (auto &m : c->models)
+            if (m.d_block) cudaFree(m.d_block);
+        c->img.release();
+        c->lists.release();
+        c->counters.release();
+        c->results.release();
+        c->one.release();
+    }
+    delete c;
+}
+
+extern "C" const char *paradl_last_error(const paradl_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
+extern "C" const char *paradl_version(void) { return "paradl-b200 1.0 (sm_100a)"; }
+
+extern "C" int32_t paradl_struct_size(int32_t which) {
+    switch (which) {
+    case 0: return (int32_t)sizeof(paradl_layer);
+    case 1: return (int32_t)sizeof(paradl_system);
+    case 2: return (int32_t)sizeof(paradl_subsweep);
+    case 3: return (int32_t)sizeof(paradl_config);
+    case 4: return (int32_t)sizeof(paradl_prediction);
+    case 5: return (int32_t)sizeof(paradl_hit);
+    default: return -1;
+    }
+}
+
+// ------------------------------------------------------------------ model
+static paradl_status validate_row(paradl_ctx *c, const paradl_layer &r, int l) {
+    if (r.kind < PARADL_CONV || r.kind > PARADL_NORM) return fail(c, PARADL_EINVAL, "row %d: bad kind %d", l, r.kind);
+    if (r.ndim < 1 || r.ndim > 3) return fail(c, PARADL_EINVAL, "row %d: ndim must be 1..3", l);
+    if (r.C < 1 || r.F < 1 || r.C > INT32_MAX || r.F > INT32_MAX)
+        return fail(c, PARADL_EINVAL, "row %d: C, F must be in [1, 2^31)", l);
+    __int128 px = 1, py = 1, pk = 1;
+    for (int a = 0; a < 3; a++) {
+        if (r.X[a] < 1 || r.Y[a] < 1 || r.X[a] > INT32_MAX || r.Y[a] > INT32_MAX)
+            return fail(c, PARADL_EINVAL, "row %d: non-positive or huge extent on axis %d", l, a);
+        if (r.K[a] < 0 || r.K[a] > INT32_MAX) return fail(c, PARADL_EINVAL, "row %d: bad kernel extent", l);
+        if (a >= r.ndim && (r.X[a] != 1 || r.Y[a] != 1))
+            return fail(c, PARADL_EINVAL, "row %d: unused axis %d must have extent 1", l, a);
+        px *= r.X[a];
+        py *= r.Y[a];
+        pk *= r.K[a];
+    }
+    if (r.x != (__int128)r.C * px) return fail(c, PARADL_EINVAL, "row %d: x != C*prod(X)", l);
+    if (r.y != (__int128)r.F * py) return fail(c, PARADL_EINVAL, "row %d: y != F*prod(Y)", l);
+    if (r.w < 0 || r.bi < 0 || r.fw < 0 || r.bw < 0 || r.wu < 0)
+        return fail(c, PARADL_EINVAL, "row %d: negative count", l);
+    const bool weighted = r.kind == PARADL_CONV || r.kind == PARADL_FC;
+    if (weighted && !(r.flags & PARADL_FLAG_FOLDED) && r.w != (__int128)r.C * r.F * pk)
+        return fail(c, PARADL_EINVAL, "row %d: w != C*F*prod(K) (set PARADL_FLAG_FOLDED for folded rows)", l);
+    if (!weighted && r.w != 0) return fail(c, PARADL_EINVAL, "row %d: weightless kind with w != 0 (P:181)", l);
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_load_model(paradl_ctx *c, const paradl_layer *rows, int32_t G, int64_t D,
+                                           int32_t *model_id) {
+    if (!c) return PARADL_EINVAL;
+    if (!rows || G < 1 || !model_id) return fail(c, PARADL_EINVAL, "need rows, G >= 1 and model_id");
+    if (G > 4096) return fail(c, PARADL_EINVAL, "G > 4096 rows is not supported");
+    if (D < 1) return fail(c, PARADL_EINVAL, "dataset size D must be >= 1");
+    HostModel m;
+    m.rows.assign(rows, rows + G);
+    m.D = D;
+    for (int l = 0; l < G; l++) {
+        paradl_status st = validate_row(c, rows[l], l);
+        if (st) return st;
+        const paradl_layer &r = rows[l];
+        m.FB += (__int128)r.fw + r.bw;
+        m.XY += (__int128)r.x + r.y;
+        m.W += r.w;
+        m.BI += r.bi;
+        m.Ysum += r.y;
+        m.Ymax = std::max<__int128>(m.Ymax, r.y);
+        for (int a = 0; a < 3; a++) m.Hmax = std::max<__int128>(m.Hmax, r.K[a] / 2);
+    }
+    if (m.FB > kLimit || m.XY > kLimit || m.W > kLimit)
+        return fail(c, PARADL_EOVERFLOW, "model sums exceed 2^62");
+    // block layout
+    ModelHdr L{};
+    size_t off = sizeof(ModelHdr);
+    L.off_geo = (uint32_t)off;
+    off = align16(off + sizeof(RowGeo) * G);
+    const size_t arr = align16(sizeof(int64_t) * (G + 1));
+    L.off_pf = (uint32_t)off; off += arr;
+    L.off_pb = (uint32_t)off; off += arr;
+    L.off_pu = (uint32_t)off; off += arr;
+    L.off_pw = (uint32_t)off; off += arr;
+    L.off_pxy = (uint32_t)off; off += arr;
+    L.off_pbi = (uint32_t)off; off += arr;
+    L.off_y = (uint32_t)off; off += align16(sizeof(int64_t) * G);
+    L.bytes = (uint32_t)off;
+    L.G = G;
+    L.D = D;
+    m.layout = L;
+    if (c->device >= 0) {
+        CUDA_TRY(c, cudaSetDevice(c->device));
+        paradl_layer *d_rows = nullptr;
+        CUDA_TRY(c, cudaMalloc(&d_rows, sizeof(paradl_layer) * G));
+        cudaError_t e = cudaMalloc(&m.d_block, L.bytes);
+        if (e == cudaSuccess) e = cudaMemcpy(d_rows, rows, sizeof(paradl_layer) * G, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = launch_prep_model(d_rows, G, D, m.d_block, L, 0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaFree(d_rows);
+        if (e != cudaSuccess) {
+            if (m.d_block) cudaFree(m.d_block);
+            return fail(c, PARADL_ECUDA, "model prep: %s", cudaGetErrorString(e));
+        }
+    }
+    c->models.push_back(std::move(m));
+    c->models_epoch++;
+    *model_id = (int32_t)c->models.size() - 1;
+    return PARADL_OK;
+}
+
+// ------------------------------------------------------------------ system
+static bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+extern "C" paradl_status paradl_set_system(paradl_ctx *c, const paradl_system *s) {
+    if (!c) return PARADL_EINVAL;
+    if (!s) return fail(c, PARADL_EINVAL, "null system");
+    if (s->n_tiers < 1 || s->n_tiers > PARADL_MAX_TIERS) return fail(c, PARADL_EINVAL, "n_tiers must be 1..%d", PARADL_MAX_TIERS);
+    for (int t = 0; t < s->n_tiers; t++) {
+        if (s->tiers[t].max_pes < 1 || (t > 0 && s->tiers[t].max_pes <= s->tiers[t - 1].max_pes))
+            return fail(c, PARADL_EINVAL, "tier max_pes must be >= 1 and strictly increasing");
+        if (!(std::isfinite(s->tiers[t].alpha_s) && s->tiers[t].alpha_s >= 0.0) || !finite_pos(s->tiers[t].beta_s_per_B))
+            return fail(c, PARADL_EINVAL, "tier %d: need alpha >= 0 and beta > 0", t);
+    }
+    if (s->delta != 2 && s->delta != 4 && s->delta != 8) return fail(c, PARADL_EINVAL, "delta must be 2, 4 or 8");
+    if (!finite_pos(s->flops_per_s) || !finite_pos(s->hbm_bytes)) return fail(c, PARADL_EINVAL, "R and capacity must be > 0");
+    if (!(s->gamma > 0.0 && s->gamma <= 1.0)) return fail(c, PARADL_EINVAL, "gamma must be in (0,1]");
+    if (!(std::isfinite(s->phi_df) && s->phi_df >= 1.0)) return fail(c, PARADL_EINVAL, "phi_df must be >= 1");
+    if (!(std::isfinite(s->tree_threshold_B) && s->tree_threshold_B >= 0.0) || s->tree_chunks < 1)
+        return fail(c, PARADL_EINVAL, "tree_threshold >= 0 and tree_chunks >= 1 required");
+    c->sys = *s;
+    c->have_system = true;
+    c->img_epoch = ~0ull;
+    return PARADL_OK;
+}
+
+// ------------------------------------------------------------------ sweep planning
+namespace {
+
+struct SubPlan {
+    SubHdr hdr{};
+    int family = 0, model = 0;   // model = ctx model id
+};
+
+struct Plan {
+    std::vector<SubPlan> subs;
+    std::vector<int> model_ids;   // image model index -> ctx model id
+    uint64_t total = 0;
+    std::vector<uint8_t> image;   // host image without model blocks (blocks appended on device)
+    uint32_t bytes = 0;           // total image bytes incl. model blocks
+};
+
+uint64_t binom_u64(int64_t n, int64_t k) {
+    if (k < 0 || k > n) return 0;
+    if (k > n - k) k = n - k;
+    unsigned __int128 r = 1;
+    for (int64_t i = 1; i <= k; i++) r = r * (unsigned __int128)(n - k + i) / (unsigned __int128)i;
+    return (uint64_t)r;
+}
+
+}  // namespace
+
+static paradl_status plan_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, Plan &P) {
+    if (!spec || spec->n_sub < 1 || !spec->sub) return fail(c, PARADL_EINVAL, "empty sweep spec");
+    if (spec->n_sub > kMaxSub) return fail(c, PARADL_EINVAL, "at most %d sub-sweeps", kMaxSub);
+    if (!c->have_system) return fail(c, PARADL_ESTATE, "paradl_set_system not called");
+    const paradl_system &sy = c->sys;
+    const int NT = sy.n_tiers;
+    // value tables are appended after the headers
+    std::vector<uint8_t> tab;
+    auto put = [&](const void *src, size_t bytes) -> uint32_t {
+        size_t off = align16(tab.size());
+        tab.resize(off + align16(bytes ? bytes : 8), 0);
+        if (bytes) memcpy(tab.data() + off, src, bytes);
+        return (uint32_t)off;
+    };
+    unsigned __int128 total = 0;
+    for (int i = 0; i < spec->n_sub; i++) {
+        const paradl_subsweep &s = spec->sub[i];
+        SubPlan sp;
+        SubHdr &h = sp.hdr;
+        if (s.family < 0 || s.family >= PARADL_N_FAMILIES) return fail(c, PARADL_EINVAL, "sub %d: bad family", i);
+        if (s.model_id < 0 || s.model_id >= (int)c->models.size())
+            return fail(c, PARADL_ESTATE, "sub %d: unknown model id %d", i, s.model_id);
+        const HostModel &m = c->models[s.model_id];
+        const int G = (int)m.rows.size();
+        const int fam = s.family;
+        const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD;
+        const bool spatial = fam == PARADL_SPATIAL || fam == PARADL_DS;
+        if (s.n_cap < 0 || s.n_flops < 0 || s.n_b < 1 || s.n_S < 0 || s.n_dims < 0 || s.n_Ls < 0 || s.n_alpha < 0 ||
+            s.n_beta < 0)
+            return fail(c, PARADL_EINVAL, "sub %d: negative list length or empty b list", i);
+        if ((s.n_cap && !s.cap) || (s.n_flops && !s.flops) || !s.b || (s.n_S && !s.S) || (s.n_dims && !s.dims) ||
+            (s.n_Ls && !s.Ls) || (s.n_alpha && !s.alpha) || (s.n_beta && !s.beta))
+            return fail(c, PARADL_EINVAL, "sub %d: null list pointer", i);
+        if (spatial && s.n_Ls < 1) return fail(c, PARADL_EINVAL, "sub %d: spatial families need an Ls list", i);
+        // materialise every list (defaults for empty ones)
+        std::vector<double> cap(s.cap, s.cap + s.n_cap), fl(s.flops, s.flops + s.n_flops);
+        if (cap.empty()) cap.push_back(sy.hbm_bytes);
+        if (fl.empty()) fl.push_back(sy.flops_per_s);
+        for (double v : cap) if (!finite_pos(v)) return fail(c, PARADL_EINVAL, "sub %d: capacity must be > 0", i);
+        for (double v : fl) if (!finite_pos(v)) return fail(c, PARADL_EINVAL, "sub %d: flops must be > 0", i);
+        std::vector<int64_t> bl(s.b, s.b + s.n_b);
+        int64_t bmax = 0;
+        for (int64_t v : bl) {
+            if (v < 1 || v > ((int64_t)1 << 40)) return fail(c, PARADL_EINVAL, "sub %d: batch out of range", i);
+            bmax = std::max(bmax, v);
+        }
+        std::vector<int32_t> Sl(s.S, s.S + s.n_S);
+        if (Sl.empty()) Sl.push_back(1);
+        for (int32_t v : Sl) if (v < 1) return fail(c, PARADL_EINVAL, "sub %d: S must be >= 1", i);
+        std::vector<int32_t> dl(s.dims, s.dims + 4 * (size_t)s.n_dims);
+        if (dl.empty()) dl = {1, 1, 1, 1};
+        int64_t degmax = 1, pmax = 1;
+        for (size_t j = 0; j < dl.size(); j += 4) {
+            const int32_t *d = &dl[j];
+            for (int a = 0; a < 4; a++)
+                if (d[a] < 1 || d[a] > (1 << 24)) return fail(c, PARADL_EINVAL, "sub %d: dims must be in [1, 2^24]", i);
+            bool ok = true;
+            switch (fam) {
+            case PARADL_SERIAL: case PARADL_PIPELINE: case PARADL_LAYERPURE:
+                ok = d[0] == 1 && d[1] == 1 && d[2] == 1 && d[3] == 1; break;
+            case PARADL_DATA: case PARADL_FILTER: case PARADL_CHANNEL: case PARADL_PD:
+                ok = d[1] == 1 && d[2] == 1 && d[3] == 1; break;
+            case PARADL_DF: ok = d[2] == 1 && d[3] == 1; break;
+            case PARADL_SPATIAL: ok = d[0] == 1; break;
+            default: break;
+            }
+            if (!ok) return fail(c, PARADL_EINVAL, "sub %d: dims tuple does not fit the family", i);
+            const int64_t deg = (fam == PARADL_DATA || fam == PARADL_DF || fam == PARADL_DS || fam == PARADL_PD) ? d[0] : 1;
+            degmax = std::max(degmax, deg);
+            pmax = std::max<int64_t>(pmax, (int64_t)d[0] * d[1] * d[2] * d[3]);
+        }
+        std::vector<int32_t> Ll(s.Ls, s.Ls + s.n_Ls);
+        if (Ll.empty()) Ll.push_back(0);
+        for (int32_t v : Ll) if (v < 0) return fail(c, PARADL_EINVAL, "sub %d: Ls must be >= 0", i);
+        std::vector<double> al, be;
+        if (s.n_alpha) al.assign(s.alpha, s.alpha + (size_t)s.n_alpha * NT);
+        else for (int t = 0; t < NT; t++) al.push_back(sy.tiers[t].alpha_s);
+        if (s.n_beta) be.assign(s.beta, s.beta + (size_t)s.n_beta * NT);
+        else for (int t = 0; t < NT; t++) be.push_back(sy.tiers[t].beta_s_per_B);
+        for (double v : al) if (!(std::isfinite(v) && v >= 0.0)) return fail(c, PARADL_EINVAL, "sub %d: alpha must be >= 0", i);
+        for (double v : be) if (!finite_pos(v)) return fail(c, PARADL_EINVAL, "sub %d: beta must be > 0", i);
+        // partition radix
+        uint64_t part_n = 1;
+        h.part_mode = s.part_mode;
+        h.s_min = h.s_max = 1;
+        std::vector<uint64_t> sblk, binom;
+        if (!pipe) {
+            if (s.part_mode != PARADL_PART_NONE) return fail(c, PARADL_EINVAL, "sub %d: partition mode on a non-pipeline family", i);
+        } else if (s.part_mode == PARADL_PART_MASK) {
+            if (G > 64) return fail(c, PARADL_EINVAL, "sub %d: mask mode needs G <= 64", i);
+            part_n = (uint64_t)1 << (G - 1);
+            h.s_min = 1;
+            h.s_max = G;
+        } else if (s.part_mode == PARADL_PART_COMB) {
+            if (s.s_min < 1 || s.s_max < s.s_min || s.s_max > G) return fail(c, PARADL_EINVAL, "sub %d: need 1 <= s_min <= s_max <= G", i);
+            if (s.s_max - 1 > kMaxCuts) return fail(c, PARADL_EINVAL, "sub %d: combination mode supports s_max <= %d", i, kMaxCuts + 1);
+            h.s_min = s.s_min;
+            h.s_max = s.s_max;
+            h.kmax = s.s_max - 1;
+            unsigned __int128 acc = 0;
+            sblk.push_back(0);
+            for (int st = s.s_min; st <= s.s_max; st++) {
+                acc += binom_u64(G - 1, st - 1);
+                if (acc >> 63) return fail(c, PARADL_EOVERFLOW, "sub %d: too many partitions", i);
+                sblk.push_back((uint64_t)acc);
+            }
+            part_n = (uint64_t)acc;
+            h.binom_stride = h.kmax + 1;
+            binom.resize((size_t)G * h.binom_stride);
+            for (int n = 0; n < G; n++)
+                for (int j = 0; j <= h.kmax; j++) binom[(size_t)n * h.binom_stride + j] = binom_u64(n, j);
+        } else {
+            return fail(c, PARADL_EINVAL, "sub %d: pipeline families need a partition mode", i);
+        }
+        // overflow proofs for every int64 intermediate of the kernels
+        {
+            const __int128 B = (__int128)bmax * degmax, dl_ = sy.delta;
+            const __int128 hv = 6 * m.Hmax * m.XY;
+            const __int128 terms[] = {B * m.FB, 2 * B * m.XY, B * dl_ * m.Ysum, (__int128)bmax * dl_ * hv,
+                                      dl_ * m.W, 2 * (__int128)bmax * m.XY + 2 * m.W + m.BI,
+                                      dl_ * (__int128)bmax * m.Ysum, (__int128)m.D};
+            for (__int128 t : terms)
+                if (t < 0 || t >= kLimit) return fail(c, PARADL_EOVERFLOW, "sub %d: an int64 intermediate may exceed 2^62", i);
+            if (pmax > ((int64_t)1 << 40)) return fail(c, PARADL_EOVERFLOW, "sub %d: PE count too large", i);
+        }
+        // image model index
+        int mi = -1;
+        for (size_t q = 0; q < P.model_ids.size(); q++)
+            if (P.model_ids[q] == s.model_id) mi = (int)q;
+        if (mi < 0) {
+            if ((int)P.model_ids.size() >= kMaxModelsPerSweep) return fail(c, PARADL_EINVAL, "at most %d models per sweep", kMaxModelsPerSweep);
+            P.model_ids.push_back(s.model_id);
+            mi = (int)P.model_ids.size() - 1;
+        }
+        h.family = fam;
+        h.model = mi;
+        h.G = G;
+        h.radix[D_BETA] = (uint32_t)(be.size() / NT);
+        h.radix[D_ALPHA] = (uint32_t)(al.size() / NT);
+        h.radix[D_LS] = (uint32_t)Ll.size();
+        h.radix[D_DIMS] = (uint32_t)(dl.size() / 4);
+        h.radix[D_S] = (uint32_t)Sl.size();
+        h.radix[D_PART] = 0;
+        h.radix[D_B] = (uint32_t)bl.size();
+        h.radix[D_FLOPS] = (uint32_t)fl.size();
+        h.radix[D_CAP] = (uint32_t)cap.size();
+        h.part_n = part_n;
+        unsigned __int128 cnt = part_n;
+        for (int d = 0; d < kDigits; d++)
+            if (d != D_PART) cnt *= h.radix[d];
+        if (cnt >> 63) return fail(c, PARADL_EOVERFLOW, "sub %d: more than 2^63 configurations", i);
+        h.count = (uint64_t)cnt;
+        h.offset = (uint64_t)total;
+        total += cnt;
+        if (total >> 63) return fail(c, PARADL_EOVERFLOW, "sweep larger than 2^63 configurations");
+        h.off_cap = put(cap.data(), cap.size() * 8);
+        h.off_flops = put(fl.data(), fl.size() * 8);
+        h.off_b = put(bl.data(), bl.size() * 8);
+        h.off_S = put(Sl.data(), Sl.size() * 4);
+        h.off_dims = put(dl.data(), dl.size() * 4);
+        h.off_Ls = put(Ll.data(), Ll.size() * 4);
+        h.off_alpha = put(al.data(), al.size() * 8);
+        h.off_beta = put(be.data(), be.size() * 8);
+        h.off_binom = put(binom.data(), binom.size() * 8);
+        h.off_sblk = put(sblk.data(), sblk.size() * 8);
+        sp.family = fam;
+        sp.model = s.model_id;
+        P.subs.push_back(sp);
+    }
+    P.total = (uint64_t)total;
+    // assemble: [ImgHdr][SubHdr...][tables][model blocks]
+    const size_t hdr_bytes = sizeof(ImgHdr) + sizeof(SubHdr) * P.subs.size();
+    ImgHdr H{};
+    H.n_sub = (int32_t)P.subs.size();
+    H.n_models = (int32_t)P.model_ids.size();
+    H.n_tiers = NT;
+    H.delta = sy.delta;
+    H.tree_chunks = sy.tree_chunks;
+    H.gamma = sy.gamma;
+    H.phi_df = sy.phi_df;
+    H.tree_thr = sy.tree_threshold_B;
+    for (int t = 0; t < PARADL_MAX_TIERS; t++) H.max_pes[t] = t < NT ? sy.tiers[t].max_pes : 0;
+    size_t off = align16(hdr_bytes + tab.size());
+    for (size_t q = 0; q < P.model_ids.size(); q++) {
+        H.model_off[q] = (uint32_t)off;
+        off += align16(c->models[P.model_ids[q]].layout.bytes);
+    }
+    if (off > 0xffffffffu) return fail(c, PARADL_ENOMEM, "image too large");
+    P.bytes = (uint32_t)off;
+    H.bytes = P.bytes;
+    for (size_t q = 0; q < P.subs.size(); q++) {
+        H.sub_off[q] = (uint32_t)(sizeof(ImgHdr) + sizeof(SubHdr) * q);
+        SubHdr &h = P.subs[q].hdr;
+        for (uint32_t *o : {&h.off_cap, &h.off_flops, &h.off_b, &h.off_S, &h.off_dims, &h.off_Ls, &h.off_alpha,
+                            &h.off_beta, &h.off_binom, &h.off_sblk})
+            *o += (uint32_t)hdr_bytes;
+    }
+    P.image.assign(align16(hdr_bytes + tab.size()), 0);
+    memcpy(P.image.data(), &H, sizeof H);
+    for (size_t q = 0; q < P.subs.size(); q++)
+        memcpy(P.image.data() + sizeof(ImgHdr) + sizeof(SubHdr) * q, &P.subs[q].hdr, sizeof(SubHdr));
+    memcpy(P.image.data() + hdr_bytes, tab.data(), tab.size());
+    return PARADL_OK;
+}
+
+static paradl_status need_device(paradl_ctx *c) {
+    if (!c) return PARADL_EINVAL;
+    c->stat_h2d = c->stat_d2h = c->stat_launches = 0;
+    if (c->device < 0) return fail(c, PARADL_ESTATE, "host-only context: no CUDA device (no CPU fallback exists)");
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, PARADL_ECUDA, "cudaSetDevice failed");
+    return PARADL_OK;
+}
+
+// Uploads the image (skipped when identical to the one already on the device).
+static paradl_status upload(paradl_ctx *c, const Plan &P, cudaStream_t st) {
+    if (P.bytes + sweep_smem_extra() > c->smem_optin)
+        return fail(c, PARADL_ENOMEM, "sweep image of %u bytes does not fit shared memory (%zu available)", P.bytes,
+                    c->smem_optin - sweep_smem_extra());
+    bool same = c->img_epoch == c->models_epoch && c->last_img == P.image && c->img.n >= P.bytes;
+    if (same) return PARADL_OK;
+    CUDA_TRY(c, c->img.ensure(P.bytes));
+    uint8_t *d = (uint8_t *)c->img.p;
+    CUDA_TRY(c, cudaMemcpyAsync(d, P.image.data(), P.image.size(), cudaMemcpyHostToDevice, st));
+    c->stat_h2d += P.image.size();
+    const ImgHdr *H = reinterpret_cast<const ImgHdr *>(P.image.data());
+    for (size_t q = 0; q < P.model_ids.size(); q++) {
+        const HostModel &m = c->models[P.model_ids[q]];
+        CUDA_TRY(c, cudaMemcpyAsync(d + H->model_off[q], m.d_block, m.layout.bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    c->last_img = P.image;
+    c->img_epoch = c->models_epoch;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_sweep_size(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t *n) {
+    if (!c || !n) return PARADL_EINVAL;
+    Plan P;
+    paradl_status st = plan_sweep(c, spec, P);
+    if (st) return st;
+    *n = P.total;
+    return PARADL_OK;
+}
+
+// mixed-radix digits of the lane stride 32 for one sub-sweep
+static void stride_digits(const SubHdr &h, LaunchArgs &a) {
+    uint64_t rem = 32;
+    a.inc_top = -1;
+    for (int d = 0; d < kDigits; d++) {
+        if (d == D_PART) {
+            a.inc_part = rem % h.part_n;
+            rem /= h.part_n;
+            if (a.inc_part) a.inc_top = d;
+        } else {
+            a.inc[d] = (uint32_t)(rem % h.radix[d]);
+            rem /= h.radix[d];
+            if (a.inc[d]) a.inc_top = d;
+        }
+    }
+}
+
+// Launches the sweep kernels for every sub-sweep intersecting [first, first+count).
+static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uint64_t count, int shard, int n_shards,
+                               bool dense, int k, const paradl_dense_out *out, cudaStream_t st, int *n_launch_out,
+                               int *grid_out) {
+    const size_t smem = P.bytes + sweep_smem_extra();
+    std::vector<LaunchArgs> launches;
+    std::vector<int> fams, grids;
+    for (size_t q = 0; q < P.subs.size(); q++) {
+        const SubHdr &h = P.subs[q].hdr;
+        const uint64_t s0 = h.offset, s1 = h.offset + h.count;
+        const uint64_t r0 = std::max(s0, first), r1 = std::min(s1, first + count);
+        if (r0 >= r1) continue;
+        LaunchArgs a{};
+        a.sub = (int32_t)q;
+        a.lo = r0 - s0;
+        a.hi = r1 - s0;
+        a.first = first;
+        a.g_range_lo = first;
+        a.g_range_hi = first + count;
+        stride_digits(h, a);
+        const int nb = max_blocks_per_sm(P.subs[q].family, dense, smem);
+        if (nb < 1) return fail(c, PARADL_ECUDA, "kernel cannot be resident with %zu bytes of shared memory", smem);
+        int grid = c->n_sm * nb;
+        const uint64_t range = a.hi - a.lo;
+        const uint64_t warps = (uint64_t)grid * kWarps;
+        // >= ~8 tiles per warp for balance, 32..32768 indices per tile
+        uint64_t steps = range / (32ull * warps * 8ull);
+        steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
+        a.steps = (uint32_t)steps;
+        const uint64_t ts = 32ull * steps;
+        a.n_tiles = (range + ts - 1) / ts;
+        const uint64_t my_tiles = a.n_tiles > (uint64_t)shard ? (a.n_tiles - shard + n_shards - 1) / n_shards : 0;
+        const uint64_t need_ctas = (my_tiles + kWarps - 1) / kWarps;
+        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, need_ctas));
+        a.shard = shard;
+        a.n_shards = n_shards;
+        a.k = k;
+        if (dense) {
+            a.t_iter = out->t_iter;
+            a.mem = out->mem;
+            a.bits = out->feasible_bits;
+            a.reason = out->reason;
+        }
+        launches.push_back(a);
+        fams.push_back(P.subs[q].family);
+        grids.push_back(grid);
+    }
+    // scratch: tile counters, per-CTA lists, feasible count
+    const size_t nl = launches.size();
+    size_t total_ctas = 0;
+    for (int g : grids) total_ctas += g;
+    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 1)));
+    if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * std::max<size_t>(1, total_ctas) * k));
+    unsigned long long *ctr = (unsigned long long *)c->counters.p;
+    CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
+    size_t cta_off = 0;
+    for (size_t i = 0; i < nl; i++) {
+        LaunchArgs &a = launches[i];
+        a.img = (const uint8_t *)c->img.p;
+        a.img_bytes = P.bytes;
+        a.tile_counter = ctr + i;
+        a.count = ctr + nl;
+        a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
+        CUDA_TRY(c, launch_sweep(fams[i], dense, a, grids[i], smem, st));
+        c->stat_launches++;
+        cta_off += grids[i];
+    }
+    if (n_launch_out) *n_launch_out = (int)nl;
+    if (grid_out) *grid_out = (int)total_ctas;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
+                                      const paradl_dense_out *out, void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (!out) return fail(c, PARADL_EINVAL, "null dense output");
+    Plan P;
+    s = plan_sweep(c, spec, P);
+    if (s) return s;
+    if (first > P.total || count > P.total - first) return fail(c, PARADL_ERANGE, "range outside the sweep (%llu configs)", (unsigned long long)P.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = upload(c, P, st);
+    if (s) return s;
+    if (count == 0) return PARADL_OK;
+    if (out->feasible_bits) CUDA_TRY(c, cudaMemsetAsync(out->feasible_bits, 0, sizeof(uint32_t) * ((count + 31) / 32), st));
+    return run_sweep(c, P, first, count, 0, 1, true, 0, out, st, nullptr, nullptr);
+}
+
+extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
+                                           int32_t shard, int32_t n_shards, int32_t k, paradl_hit *d_hits,
+                                           uint64_t *d_n_feasible, void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (k < 1 || k > PARADL_MAX_TOPK) return fail(c, PARADL_EINVAL, "k must be in 1..%d", PARADL_MAX_TOPK);
+    if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(c, PARADL_EINVAL, "bad shard / n_shards");
+    if (!d_hits || !d_n_feasible) return fail(c, PARADL_EINVAL, "null output");
+    Plan P;
+    s = plan_sweep(c, spec, P);
+    if (s) return s;
+    if (first > P.total || count > P.total - first) return fail(c, PARADL_ERANGE, "range outside the sweep (%llu configs)", (unsigned long long)P.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = upload(c, P, st);
+    if (s) return s;
+    int nl = 0, ctas = 0;
+    s = run_sweep(c, P, first, count, shard, n_shards, false, k, nullptr, st, &nl, &ctas);
+    if (s) return s;
+    unsigned long long *ctr = (unsigned long long *)c->counters.p;
+    if (nl == 0) {
+        CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long)));
+        ctr = (unsigned long long *)c->counters.p;
+        CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+    }
+    CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nl ? ctas : 0, k, ctr + nl, 1, d_hits,
+                             (unsigned long long *)d_n_feasible, st));
+    c->stat_launches++;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_merge_topk(paradl_ctx *c, const paradl_hit *d_lists, int32_t n_lists, int32_t k,
+                                           const uint64_t *d_counts, paradl_hit *d_out, uint64_t *d_count_out,
+                                           void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (k < 1 || k > PARADL_MAX_TOPK || n_lists < 0 || (n_lists && (!d_lists || !d_counts)) || !d_out || !d_count_out)
+        return fail(c, PARADL_EINVAL, "bad merge arguments");
+    CUDA_TRY(c, launch_merge(d_lists, n_lists, k, (const unsigned long long *)d_counts, n_lists, d_out,
+                             (unsigned long long *)d_count_out, (cudaStream_t)stream));
+    c->stat_launches++;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_topk(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
+                                     int32_t k, paradl_hit *hits, uint64_t *n_feasible, void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (!hits || !n_feasible) return fail(c, PARADL_EINVAL, "null output");
+    if (k < 1 || k > PARADL_MAX_TOPK) return fail(c, PARADL_EINVAL, "k must be in 1..%d", PARADL_MAX_TOPK);
+    CUDA_TRY(c, c->results.ensure(sizeof(paradl_hit) * PARADL_MAX_TOPK + 16));
+    paradl_hit *dh = (paradl_hit *)c->results.p;
+    uint64_t *dc = (uint64_t *)((uint8_t *)c->results.p + sizeof(paradl_hit) * PARADL_MAX_TOPK);
+    s = paradl_topk_async(c, spec, first, count, 0, 1, k, dh, dc, stream);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(c, cudaMemcpyAsync(hits, dh, sizeof(paradl_hit) * k, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaMemcpyAsync(n_feasible, dc, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    c->stat_d2h += sizeof(paradl_hit) * k + sizeof(uint64_t);
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_argmin(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
+                                       paradl_hit *best, uint64_t *n_feasible, void *stream) {
+    return paradl_topk(c, spec, first, count, 1, best, n_feasible, stream);
+}
+
+static paradl_status explain_impl(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t idx, paradl_config *cfg,
+                                  paradl_prediction *pred) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    Plan P;
+    s = plan_sweep(c, spec, P);
+    if (s) return s;
+    if (idx >= P.total) return fail(c, PARADL_ERANGE, "index %llu outside the sweep", (unsigned long long)idx);
+    s = upload(c, P, 0);
+    if (s) return s;
+    int sub = 0;
+    while (idx >= P.subs[sub].hdr.offset + P.subs[sub].hdr.count) sub++;
+    CUDA_TRY(c, c->one.ensure(sizeof(paradl_config) + sizeof(paradl_prediction)));
+    paradl_config *dcfg = (paradl_config *)c->one.p;
+    paradl_prediction *dpr = (paradl_prediction *)((uint8_t *)c->one.p + sizeof(paradl_config));
+    CUDA_TRY(c, launch_explain((const uint8_t *)c->img.p, P.bytes, sub, idx - P.subs[sub].hdr.offset, dcfg, dpr, 0));
+    paradl_config hc;
+    paradl_prediction hp;
+    CUDA_TRY(c, cudaMemcpy(&hc, dcfg, sizeof hc, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(&hp, dpr, sizeof hp, cudaMemcpyDeviceToHost));
+    if (cfg) *cfg = hc;
+    if (pred) *pred = hp;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_decode(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t idx, paradl_config *out) {
+    if (!out) return fail(c, PARADL_EINVAL, "null output");
+    return explain_impl(c, spec, idx, out, nullptr);
+}
+
+extern "C" paradl_status paradl_explain(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t idx,
+                                        paradl_prediction *out) {
+    if (!out) return fail(c, PARADL_EINVAL, "null output");
+    return explain_impl(c, spec, idx, nullptr, out);
+}
+
+extern "C" uint64_t paradl_stat(const paradl_ctx *c, int32_t which) {
+    if (!c) return 0;
+    switch (which) {
+    case 0: return c->stat_h2d;
+    case 1: return c->stat_d2h;
+    case 2: return c->stat_launches;
+    default: return 0;
+    }
+}
+
+extern "C" paradl_status paradl_fp64_peak(paradl_ctx *c, double ms, double *inst_per_s) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (!inst_per_s || !(ms > 0)) return fail(c, PARADL_EINVAL, "bad arguments");
+    double *sink = nullptr;
+    CUDA_TRY(c, cudaMalloc(&sink, 256 * sizeof(double)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int threads = 0;
+    int iters = 64;
+    float el = 0.f;
+    cudaError_t e = cudaSuccess;
+    for (int round = 0; round < 12; round++) {   // grow until the launch lasts ~ms
+        e = launch_fp64_bench(c->n_sm, iters, sink, 0, &threads);
+        if (e != cudaSuccess) break;
+        cudaEventRecord(e0, 0);
+        e = launch_fp64_bench(c->n_sm, iters, sink, 0, &threads);
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&el, e0, e1);
+        if (e != cudaSuccess || el >= ms) break;
+        iters *= 2;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (e != cudaSuccess) return fail(c, PARADL_ECUDA, "fp64 bench: %s", cudaGetErrorString(e));
+    *inst_per_s = (double)threads * iters * 16.0 * 8.0 / (el * 1e-3);
+    return PARADL_OK;
+}

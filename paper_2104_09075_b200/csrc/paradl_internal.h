@@ -1,0 +1,109 @@
+// paradl_internal.h -- device image layout shared by the host library (api.cpp) and the
+// CUDA kernels (kernels.cu).  Not part of the public ABI (include/paradl.h).
+//
+// A sweep is evaluated from one contiguous "image" in device global memory that every
+// persistent CTA stages into shared memory with one TMA bulk copy (cp.async.bulk +
+// mbarrier):
+//
+//   [ImgHdr][SubHdr x n_sub][value tables, binomials, stage-block offsets][model blocks]
+//
+// A model block is produced on the device by the prep kernel at paradl_load_model
+// (prefix sums and totals) and copied device-to-device into the image.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "paradl.h"
+
+namespace paradl {
+
+constexpr int kMaxSub = 64;
+constexpr int kMaxModelsPerSweep = 8;
+constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
+
+// digits of the canonical mixed radix, fast -> slow
+enum { D_BETA = 0, D_ALPHA, D_LS, D_DIMS, D_S, D_PART, D_B, D_FLOPS, D_CAP, kDigits };
+
+struct RowGeo {            // 48 B: geometry of one layer row (halo / limits)
+    int32_t kind, flags;
+    int32_t C, F;
+    int32_t X[3], Y[3], K[3];
+    int32_t pad;
+};
+
+struct ModelHdr {          // 128 B, start of a model block
+    int32_t G, pad0;
+    int64_t D;
+    // per-model integer sums (Table 2 Sigma_l), computed by the prep kernel
+    int64_t FB, WU, W, BI, XY, YC, NC, Fmin, Cmin2;
+    // byte offsets from the start of the block
+    uint32_t off_geo, off_pf, off_pb, off_pu, off_pw, off_pxy, off_pbi, off_y;
+    uint32_t bytes, pad1;
+};
+static_assert(sizeof(ModelHdr) == 128, "ModelHdr layout");
+
+struct ImgHdr {
+    uint32_t bytes;
+    int32_t n_sub, n_models, n_tiers;
+    int32_t delta, tree_chunks;
+    double gamma, phi_df, tree_thr;
+    int64_t max_pes[PARADL_MAX_TIERS];
+    uint32_t model_off[kMaxModelsPerSweep];
+    uint32_t sub_off[kMaxSub];
+};
+static_assert(sizeof(ImgHdr) % 16 == 0, "ImgHdr alignment");
+
+struct SubHdr {
+    int32_t family, model;                 // model = index into ImgHdr::model_off
+    int32_t part_mode, s_min, s_max, kmax; // kmax = s_max - 1 (COMB)
+    uint32_t radix[kDigits];               // radix[D_PART] unused (see part_n)
+    int32_t G;
+    uint64_t part_n;                       // partition radix
+    uint64_t count, offset;                // configs in this sub-sweep, global index offset
+    uint32_t off_cap, off_flops, off_b, off_S, off_dims, off_Ls, off_alpha, off_beta;
+    uint32_t off_binom, off_sblk;          // uint64 C(n,j) [n*(kmax+1)+j], n < G; uint64 s-block offsets
+    uint32_t binom_stride, pad0, pad1, pad2;
+};
+static_assert(sizeof(SubHdr) % 16 == 0, "SubHdr alignment");
+
+// Arguments of one sweep-kernel launch (one sub-sweep, a local index range).
+struct LaunchArgs {
+    const uint8_t *img;            // device image
+    uint32_t img_bytes;            // multiple of 16
+    int32_t sub;
+    uint64_t lo, hi;               // local index range [lo, hi) within the sub-sweep
+    uint64_t first;                // global index of dense element 0
+    uint64_t n_tiles;
+    uint32_t steps;                // tile = 32 * steps consecutive indices
+    int32_t shard, n_shards;
+    unsigned long long *tile_counter;
+    int32_t k;
+    paradl_hit *cta_lists;         // [gridDim.x][k] (reduce mode)
+    unsigned long long *count;     // feasible count accumulator (reduce mode)
+    double *t_iter;                // dense outputs (indexed by global idx - first)
+    double *mem;
+    uint32_t *bits;
+    uint8_t *reason;
+    uint32_t inc[kDigits];         // mixed-radix digits of the lane stride 32
+    uint64_t inc_part;
+    int32_t inc_top;               // highest digit with a non-zero increment
+    uint64_t g_range_lo, g_range_hi; // global [first, first+count) (dense bit ownership)
+};
+
+// launchers implemented in kernels.cu
+cudaError_t launch_prep_model(const paradl_layer *d_rows, int32_t G, int64_t D, uint8_t *d_block,
+                              const ModelHdr &layout, cudaStream_t st);
+cudaError_t launch_sweep(int family, bool dense, const LaunchArgs &a, int grid, size_t smem,
+                         cudaStream_t st);
+int max_blocks_per_sm(int family, bool dense, size_t smem);
+size_t sweep_smem_extra();
+cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
+                         const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
+                         unsigned long long *count_out, cudaStream_t st);
+cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
+cudaError_t launch_explain(const uint8_t *img, uint32_t img_bytes, int32_t sub, uint64_t local,
+                           paradl_config *d_cfg, paradl_prediction *d_pred, cudaStream_t st);
+
+}  // namespace paradl

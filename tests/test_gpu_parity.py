@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle (-m gpu).
+
+Bar (BASELINE.json north_star): bit-exact feasibility masks, reasons, feasible counts,
+partition decodes, argmin / top-k indices (ties -> lowest index); fp64 times and memory
+within 1e-9 relative (the design target is bit-identical, so the tests
+also report how many differ at all).
+"""
+from __future__ import annotations
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from workloads import corpus
+from workloads import sweeps as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2104_09075_b200 as P   # noqa: E402
+
+REL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda:0")
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    both_inf = np.isinf(a) & np.isinf(b) & (np.sign(a) == np.sign(b))
+    d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
+    d[both_inf] = 0.0
+    d[(a == b)] = 0.0
+    return d
+
+
+def gpu_dense(ctx, spec, first, count, dev):
+    t = torch.empty(count, dtype=torch.float64, device=dev)
+    m = torch.empty(count, dtype=torch.float64, device=dev)
+    bits = torch.empty((count + 31) // 32, dtype=torch.int32, device=dev)
+    rs = torch.empty(count, dtype=torch.uint8, device=dev)
+    ctx.sweep_dense(spec, first, count, t.data_ptr(), m.data_ptr(), bits.data_ptr(), rs.data_ptr(),
+                    stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    return (t.cpu().numpy(), m.cpu().numpy(), bits.cpu().numpy().view(np.uint32), rs.cpu().numpy())
+
+
+def check_dense(ctx, spec, osw, first, count, dev):
+    t, m, bits, rs = gpu_dense(ctx, spec, first, count, dev)
+    ot, om, obits, ors = osw.dense(first, count)
+    assert np.array_equal(rs, ors), np.nonzero(rs != ors)[0][:10]
+    assert np.array_equal(bits, obits)
+    assert rel_err(t, ot).max() <= REL
+    assert rel_err(m, om).max() <= REL
+    return int(np.sum(t != ot)) + int(np.sum(m != om))
+
+
+def check_topk(ctx, spec, osw, first, count, k):
+    hits, nf = ctx.topk(spec, k, first, count)
+    ohits, onf = osw.topk(first, count, k)
+    assert nf == onf
+    assert [h[0] for h in hits] == [h[0] for h in ohits]
+    for (gi, gk), (oi, ok) in zip(hits, ohits):
+        if oi == 2 ** 64 - 1:
+            assert math.isinf(gk) and gi == oi
+        else:
+            assert abs(gk - ok) <= REL * abs(ok)
+    return hits, nf
+
+
+# ------------------------------------------------------------------ random corpora (all families)
+@pytest.mark.parametrize("seed", range(40))
+def test_random_corpus_dense_and_topk(dev, oracle_mod, seed):
+    sw = corpus.random_sweep(seed)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = ctx.sweep_size(spec)
+    assert n == osw.size()
+    diffs = check_dense(ctx, spec, osw, 0, n, dev)
+    assert diffs == 0, f"{diffs} values not bit-identical (within tolerance)"
+    for k in (1, 7, 64):
+        check_topk(ctx, spec, osw, 0, n, k)
+    rng = random.Random(seed)
+    for _ in range(3):   # ragged sub-ranges crossing sub-sweep boundaries
+        a = rng.randrange(n)
+        c = rng.randrange(n - a + 1)
+        check_dense(ctx, spec, osw, a, c, dev)
+        check_topk(ctx, spec, osw, a, c, rng.choice([1, 5, 33]))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_explain_and_decode(dev, oracle_mod, seed):
+    sw = corpus.random_sweep(seed)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    rng = random.Random(seed)
+    for idx in [0, n - 1] + [rng.randrange(n) for _ in range(40)]:
+        g = ctx.explain(spec, idx)
+        o = osw.explain(idx)
+        for f in ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_halo", "t_p2p", "t_iter", "t_epoch", "mem", "I"):
+            assert rel_err([getattr(g, f)], [getattr(o, f)])[0] <= REL, (idx, f)
+        assert g.reason == o.reason and g.feasible == o.feasible
+        gc = ctx.decode(spec, idx)
+        oc = osw.decode(idx)
+        assert gc.sub == oc.sub and gc.n_stages == oc.n_stages
+        assert list(gc.stage_end[:gc.n_stages]) == list(oc.stage_end[:oc.n_stages])
+        assert (gc.b, gc.S, gc.Ls, tuple(gc.dims)) == (oc.b, oc.S, oc.Ls, tuple(oc.dims))
+        assert gc.B == o.B and gc.p == o.p
+
+
+def test_empty_and_edge_ranges(dev, oracle_mod):
+    sw = corpus.random_sweep(3)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    hits, nf = ctx.topk(spec, 4, n, 0)
+    assert nf == 0 and all(h[0] == 2 ** 64 - 1 for h in hits)
+    check_dense(ctx, spec, osw, n - 1, 1, dev)
+    check_dense(ctx, spec, osw, 5, 31, dev)
+    check_dense(ctx, spec, osw, 3, 33, dev)
+    with pytest.raises(P.ParadlError) as e:
+        ctx.topk(spec, 4, n, 1)
+    assert e.value.status == -5
+    with pytest.raises(P.ParadlError):
+        ctx.topk(spec, 65, 0, n)
+
+
+# ------------------------------------------------------------------ BASELINE configs
+def test_config1_full(dev, oracle_mod):
+    sw = W.config1()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    assert check_dense(ctx, spec, osw, 0, 33, dev) == 0
+    hits, nf = check_topk(ctx, spec, osw, 0, 33, 33)
+    assert nf == 22 and hits[0][0] == 31
+    (best, key), nf1 = ctx.argmin(spec)
+    assert best == 31 and nf1 == 22
+
+
+def _small(cfg, **kw):
+    return W.CONFIGS[cfg](**kw) if kw else W.CONFIGS[cfg]()
+
+
+@pytest.mark.parametrize("cfg,kw", [(2, dict(n_alpha=3, n_beta=5, b_list=[1, 7, 64, 256], pipe_smax=3)),
+                                    (3, dict(n_alpha=3, n_beta=2)),
+                                    (4, dict(n_alpha=2, n_beta=3)),
+                                    (5, dict(s_max=3))])
+def test_reduced_configs(dev, oracle_mod, cfg, kw):
+    sw = _small(cfg, **kw)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    full = n <= 3_000_000
+    if full:
+        assert check_dense(ctx, spec, osw, 0, n, dev) == 0
+        check_topk(ctx, spec, osw, 0, n, 64)
+    rng = random.Random(cfg)
+    for _ in range(6):
+        a = rng.randrange(max(1, n - 100_000))
+        c = min(n - a, rng.randrange(1, 100_000))
+        check_dense(ctx, spec, osw, a, c, dev)
+        check_topk(ctx, spec, osw, a, c, 16)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_full_size_windows(dev, oracle_mod, cfg):
+    """Full BASELINE sizes: dense windows at random offsets (bench's launch configuration)
+    against the oracle's one-by-one evaluation."""
+    sw = W.CONFIGS[cfg]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    rng = random.Random(100 + cfg)
+    starts = [0, n - 4000] + [rng.randrange(n - 4000) for _ in range(10)]
+    for a in starts:
+        c = rng.randrange(1000, 4000)
+        check_dense(ctx, spec, osw, a, c, dev)
+        check_topk(ctx, spec, osw, a, c, 8)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_full_sweep_topk_properties(dev, oracle_mod, cfg):
+    """Whole-sweep top-k at full size: every hit re-evaluated by the oracle gives its key;
+    hits are feasible, sorted, and no sampled configuration beats the k-th hit; the count
+    equals the popcount of the dense feasibility bits over the same range."""
+    sw = W.CONFIGS[cfg]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    hits, nf = ctx.topk(spec, 64, 0, n)
+    keys = [h[1] for h in hits]
+    assert keys == sorted(keys)
+    idx = np.array([h[0] for h in hits], np.uint64)
+    t, m, r, key = osw.eval_many(idx)
+    assert np.all(r == 0)
+    assert rel_err(key, keys).max() <= REL
+    rng = np.random.default_rng(cfg)
+    sample = rng.integers(0, n, 200_000, dtype=np.uint64)
+    _, _, rs, ks = osw.eval_many(sample)
+    kth = (keys[-1], int(idx[-1]))
+    better = [(k_, int(i_)) for k_, i_, r_ in zip(ks, sample, rs) if r_ == 0 and (k_, int(i_)) < kth]
+    assert all(int(i_) in set(int(x) for x in idx) for _, i_ in better)
+    # count vs dense popcount (chunked)
+    tot = 0
+    chunk = 1 << 27
+    dev_bits = torch.empty((chunk + 31) // 32, dtype=torch.int32, device=dev)
+    for a in range(0, n, chunk):
+        c = min(chunk, n - a)
+        ctx.sweep_dense(spec, a, c, 0, 0, dev_bits.data_ptr(), 0, stream=torch.cuda.current_stream())
+        nw = (c + 31) // 32
+        tot += int(torch.sum(_popcount(dev_bits[:nw])))
+    assert tot == nf
+
+
+def _popcount(x):
+    x = x.to(torch.int64) & 0xFFFFFFFF
+    x = x - ((x >> 1) & 0x55555555)
+    x = (x & 0x33333333) + ((x >> 2) & 0x33333333)
+    x = (x + (x >> 4)) & 0x0F0F0F0F
+    return ((x * 0x01010101) & 0xFFFFFFFF) >> 24
+
+
+def test_sharded_topk_merge_equals_single(dev, oracle_mod):
+    sw = W.config2(n_alpha=8, n_beta=8, b_list=[2, 32, 256], pipe_smax=3)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    n = ctx.sweep_size(spec)
+    k = 32
+    single, nf = ctx.topk(spec, k)
+    for ns in (2, 3, 4, 8):
+        lists = torch.empty((ns, k, 2), dtype=torch.int64, device=dev)
+        counts = torch.zeros(ns, dtype=torch.int64, device=dev)
+        for s in range(ns):
+            ctx.topk_async(spec, 0, n, s, ns, k, lists[s].data_ptr(), counts[s:].data_ptr(),
+                           stream=torch.cuda.current_stream())
+        out = torch.empty((k, 2), dtype=torch.int64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        ctx.merge_topk(lists.data_ptr(), ns, k, counts.data_ptr(), out.data_ptr(), cnt.data_ptr(),
+                       stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        got = [int(v) for v in o[:, 0].astype(np.uint64)]
+        assert got == [h[0] for h in single]
+        assert int(cnt.item()) == nf
