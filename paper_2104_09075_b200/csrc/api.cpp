@@ -62,9 +62,13 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one;
+    DevBuf img, lists, counters, results, one, halo;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
+    std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
+    std::vector<cudaEvent_t> events;
+    cudaEvent_t fork_ev = nullptr;
+    unsigned long long *last_count_ptr = nullptr;
     uint64_t models_epoch = 0, img_epoch = ~0ull;
 };
 
@@ -124,6 +128,10 @@ extern "C" void paradl_destroy(paradl_ctx *c) {
         c->counters.release();
         c->results.release();
         c->one.release();
+        c->halo.release();
+        for (auto s2 : c->streams) cudaStreamDestroy(s2);
+        for (auto e2 : c->events) cudaEventDestroy(e2);
+        if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     }
     delete c;
 }
@@ -429,6 +437,10 @@ static paradl_status plan_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, Pl
         h.radix[D_FLOPS] = (uint32_t)fl.size();
         h.radix[D_CAP] = (uint32_t)cap.size();
         h.part_n = part_n;
+        if (spatial && (uint64_t)h.radix[D_DIMS] * h.radix[D_LS] >= (1ull << 24))
+            return fail(c, PARADL_EINVAL, "sub %d: n_dims * n_Ls must be < 2^24 for spatial families", i);
+        if ((uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] >= (1ull << 31))
+            return fail(c, PARADL_EINVAL, "sub %d: n_alpha * n_beta must be < 2^31", i);
         unsigned __int128 cnt = part_n;
         for (int d = 0; d < kDigits; d++)
             if (d != D_PART) cnt *= h.radix[d];
@@ -526,7 +538,7 @@ extern "C" paradl_status paradl_sweep_size(paradl_ctx *c, const paradl_sweep_spe
 }
 
 // mixed-radix digits of the lane stride 32 for one sub-sweep
-static void stride_digits(const SubHdr &h, LaunchArgs &a) {
+static void stride_digits(const SubHdr &h, WorkItem &a) {
     uint64_t rem = 32;
     a.inc_top = -1;
     for (int d = 0; d < kDigits; d++) {
@@ -542,75 +554,141 @@ static void stride_digits(const SubHdr &h, LaunchArgs &a) {
     }
 }
 
-// Launches the sweep kernels for every sub-sweep intersecting [first, first+count).
+// Launches the sweep for every sub-sweep intersecting [first, first+count): one persistent
+// launch per strategy family (its work items share a tile queue), all forked onto internal
+// streams so that small latency-bound families overlap each other and the big ones; the
+// caller's stream then waits for all of them.  Per-CTA top-k lists land contiguously in
+// c->lists (reduce mode); *n_lists_out = total CTAs.
 static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uint64_t count, int shard, int n_shards,
-                               bool dense, int k, const paradl_dense_out *out, cudaStream_t st, int *n_launch_out,
-                               int *grid_out) {
+                               bool dense, int k, const paradl_dense_out *out, cudaStream_t st, int *n_lists_out) {
     const size_t smem = P.bytes + sweep_smem_extra();
-    std::vector<LaunchArgs> launches;
-    std::vector<int> fams, grids;
+    std::vector<LaunchArgs> L;
+    std::vector<int> fam_of;
+    HaloJobs hj{};
+    hj.img = (const uint8_t *)c->img.p;
+    size_t halo_entries = 0;
+    if (n_lists_out) *n_lists_out = 0;
     for (size_t q = 0; q < P.subs.size(); q++) {
         const SubHdr &h = P.subs[q].hdr;
         const uint64_t s0 = h.offset, s1 = h.offset + h.count;
         const uint64_t r0 = std::max(s0, first), r1 = std::min(s1, first + count);
         if (r0 >= r1) continue;
-        LaunchArgs a{};
-        a.sub = (int32_t)q;
-        a.lo = r0 - s0;
-        a.hi = r1 - s0;
+        const int fam = P.subs[q].family;
+        size_t li = 0;
+        while (li < fam_of.size() && fam_of[li] != fam) li++;
+        if (li == fam_of.size()) {
+            fam_of.push_back(fam);
+            L.emplace_back();
+            memset(&L.back(), 0, sizeof(LaunchArgs));
+        }
+        LaunchArgs &a = L[li];
+        WorkItem &w = a.work[a.n_work++];
+        w.sub = (int32_t)q;
+        w.family = fam;
+        w.lo = r0 - s0;
+        w.hi = r1 - s0;
+        stride_digits(h, w);
+        if (fam == PARADL_SPATIAL || fam == PARADL_DS) {
+            HaloJob &j = hj.job[hj.n_jobs++];
+            j.sub = (int32_t)q;
+            j.n_entries = (int32_t)(h.radix[D_DIMS] * h.radix[D_LS]);
+            j.entry_base = (int32_t)halo_entries;
+            halo_entries += j.n_entries;
+        }
+    }
+    const size_t nl = L.size();
+    if (nl == 0) return PARADL_OK;
+    if (halo_entries > (size_t)INT32_MAX) return fail(c, PARADL_EINVAL, "halo tables too large");
+    hj.total_entries = (int32_t)halo_entries;
+    if (halo_entries) {
+        CUDA_TRY(c, c->halo.ensure(sizeof(HaloEntry) * halo_entries));
+        for (int j = 0; j < hj.n_jobs; j++) hj.job[j].tab = (HaloEntry *)c->halo.p + hj.job[j].entry_base;
+        for (auto &a : L)
+            for (int i = 0; i < a.n_work; i++)
+                for (int j = 0; j < hj.n_jobs; j++)
+                    if (hj.job[j].sub == a.work[i].sub) a.work[i].halo = hj.job[j].tab;
+    }
+    // tiles and grids
+    std::vector<int> grids(nl);
+    size_t total_ctas = 0;
+    for (size_t li = 0; li < nl; li++) {
+        LaunchArgs &a = L[li];
+        const int nb = max_blocks_per_sm(fam_of[li], dense, smem);
+        if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smem);
+        const int grid_max = c->n_sm * nb;
+        const uint64_t warps = (uint64_t)grid_max * kWarps;
+        uint64_t tiles = 0;
+        for (int i = 0; i < a.n_work; i++) {
+            WorkItem &w = a.work[i];
+            const uint64_t range = w.hi - w.lo;
+            // >= ~8 tiles per warp for balance, 32..32768 configurations per tile
+            uint64_t steps = range / (32ull * warps * 8ull);
+            steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
+            w.steps = (uint32_t)steps;
+            w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
+            w.tile_base = tiles;
+            tiles += w.n_tiles;
+        }
+        a.total_tiles = tiles;
+        const uint64_t my_tiles = tiles > (uint64_t)shard ? (tiles - shard + n_shards - 1) / n_shards : 0;
+        const uint64_t need_ctas = (my_tiles + 4ull * kWarps - 1) / (4ull * kWarps);   // >= 4 tiles per warp
+        grids[li] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid_max, need_ctas));
+        total_ctas += grids[li];
+    }
+    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 1)));
+    if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * total_ctas * k));
+    unsigned long long *ctr = (unsigned long long *)c->counters.p;
+    CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
+    if (halo_entries) {
+        CUDA_TRY(c, launch_halo_tables(hj, st));
+        c->stat_launches++;
+    }
+    // fork onto internal streams
+    const bool fork = nl > 1;
+    if (fork) {
+        while (c->streams.size() < nl) {
+            cudaStream_t s2;
+            cudaEvent_t e2;
+            CUDA_TRY(c, cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+            c->streams.push_back(s2);
+            c->events.push_back(e2);
+        }
+        if (!c->fork_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventRecord(c->fork_ev, st));
+    }
+    size_t cta_off = 0;
+    for (size_t li = 0; li < nl; li++) {
+        LaunchArgs &a = L[li];
+        a.img = (const uint8_t *)c->img.p;
+        a.img_bytes = P.bytes;
         a.first = first;
-        a.g_range_lo = first;
-        a.g_range_hi = first + count;
-        stride_digits(h, a);
-        const int nb = max_blocks_per_sm(P.subs[q].family, dense, smem);
-        if (nb < 1) return fail(c, PARADL_ECUDA, "kernel cannot be resident with %zu bytes of shared memory", smem);
-        int grid = c->n_sm * nb;
-        const uint64_t range = a.hi - a.lo;
-        const uint64_t warps = (uint64_t)grid * kWarps;
-        // >= ~8 tiles per warp for balance, 32..32768 indices per tile
-        uint64_t steps = range / (32ull * warps * 8ull);
-        steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
-        a.steps = (uint32_t)steps;
-        const uint64_t ts = 32ull * steps;
-        a.n_tiles = (range + ts - 1) / ts;
-        const uint64_t my_tiles = a.n_tiles > (uint64_t)shard ? (a.n_tiles - shard + n_shards - 1) / n_shards : 0;
-        const uint64_t need_ctas = (my_tiles + kWarps - 1) / kWarps;
-        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, need_ctas));
         a.shard = shard;
         a.n_shards = n_shards;
+        a.tile_counter = ctr + li;
+        a.count = ctr + nl;
         a.k = k;
+        a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
         if (dense) {
             a.t_iter = out->t_iter;
             a.mem = out->mem;
             a.bits = out->feasible_bits;
             a.reason = out->reason;
         }
-        launches.push_back(a);
-        fams.push_back(P.subs[q].family);
-        grids.push_back(grid);
-    }
-    // scratch: tile counters, per-CTA lists, feasible count
-    const size_t nl = launches.size();
-    size_t total_ctas = 0;
-    for (int g : grids) total_ctas += g;
-    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 1)));
-    if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * std::max<size_t>(1, total_ctas) * k));
-    unsigned long long *ctr = (unsigned long long *)c->counters.p;
-    CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
-    size_t cta_off = 0;
-    for (size_t i = 0; i < nl; i++) {
-        LaunchArgs &a = launches[i];
-        a.img = (const uint8_t *)c->img.p;
-        a.img_bytes = P.bytes;
-        a.tile_counter = ctr + i;
-        a.count = ctr + nl;
-        a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
-        CUDA_TRY(c, launch_sweep(fams[i], dense, a, grids[i], smem, st));
+        cudaStream_t ls = st;
+        if (fork) {
+            ls = c->streams[li];
+            CUDA_TRY(c, cudaStreamWaitEvent(ls, c->fork_ev, 0));
+        }
+        CUDA_TRY(c, launch_sweep(fam_of[li], dense, a, grids[li], smem, ls));
         c->stat_launches++;
-        cta_off += grids[i];
+        if (fork) CUDA_TRY(c, cudaEventRecord(c->events[li], ls));
+        cta_off += grids[li];
     }
-    if (n_launch_out) *n_launch_out = (int)nl;
-    if (grid_out) *grid_out = (int)total_ctas;
+    if (fork)
+        for (size_t li = 0; li < nl; li++) CUDA_TRY(c, cudaStreamWaitEvent(st, c->events[li], 0));
+    c->last_count_ptr = ctr + nl;
+    if (n_lists_out) *n_lists_out = (int)total_ctas;
     return PARADL_OK;
 }
 
@@ -628,7 +706,7 @@ extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *sp
     if (s) return s;
     if (count == 0) return PARADL_OK;
     if (out->feasible_bits) CUDA_TRY(c, cudaMemsetAsync(out->feasible_bits, 0, sizeof(uint32_t) * ((count + 31) / 32), st));
-    return run_sweep(c, P, first, count, 0, 1, true, 0, out, st, nullptr, nullptr);
+    return run_sweep(c, P, first, count, 0, 1, true, 0, out, st, nullptr);
 }
 
 extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
@@ -646,16 +724,17 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
     cudaStream_t st = (cudaStream_t)stream;
     s = upload(c, P, st);
     if (s) return s;
-    int nl = 0, ctas = 0;
-    s = run_sweep(c, P, first, count, shard, n_shards, false, k, nullptr, st, &nl, &ctas);
+    int nlists = 0;
+    c->last_count_ptr = nullptr;
+    s = run_sweep(c, P, first, count, shard, n_shards, false, k, nullptr, st, &nlists);
     if (s) return s;
-    unsigned long long *ctr = (unsigned long long *)c->counters.p;
-    if (nl == 0) {
-        CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long)));
-        ctr = (unsigned long long *)c->counters.p;
-        CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * 2));
+    unsigned long long *cnt = c->last_count_ptr;
+    if (nlists == 0) {
+        cnt = (unsigned long long *)c->counters.p;
+        CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     }
-    CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nl ? ctas : 0, k, ctr + nl, 1, d_hits,
+    CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
                              (unsigned long long *)d_n_feasible, st));
     c->stat_launches++;
     return PARADL_OK;

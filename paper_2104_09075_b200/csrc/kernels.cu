@@ -151,16 +151,30 @@ __device__ void succ_comb(const View &v, Lane &L, uint16_t *cuts, int cs) {
 
 __device__ void decode(const View &v, uint64_t u, Lane &L, uint16_t *cuts, int cs) {
     const SubHdr *S = v.S;
+    if ((u >> 32) == 0 && (S->part_n >> 32) == 0) {
+        // 32-bit mixed-radix decode (most sub-sweeps): ~5x cheaper than 64-bit division
+        uint32_t w = (uint32_t)u;
 #pragma unroll
-    for (int i = 0; i < kDigits; i++) {
-        if (i == D_PART) {
-            uint64_t np = S->part_n;
-            L.part = u % np;
-            u /= np;
-        } else {
-            uint32_t r = S->radix[i];
-            L.d[i] = (uint32_t)(u % r);
-            u /= r;
+        for (int i = 0; i < kDigits; i++) {
+            const uint32_t r = i == D_PART ? (uint32_t)S->part_n : S->radix[i];
+            const uint32_t q = w / r;
+            const uint32_t d = w - q * r;
+            if (i == D_PART) L.part = d;
+            else L.d[i] = d;
+            w = q;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kDigits; i++) {
+            if (i == D_PART) {
+                uint64_t np = S->part_n;
+                L.part = u % np;
+                u /= np;
+            } else {
+                uint32_t r = S->radix[i];
+                L.d[i] = (uint32_t)(u % r);
+                u /= r;
+            }
         }
     }
     L.ns = 1;
@@ -170,7 +184,7 @@ __device__ void decode(const View &v, uint64_t u, Lane &L, uint16_t *cuts, int c
 
 // Adds the lane stride (mixed-radix digits inc[]) to the digit vector; returns the
 // slowest digit that changed (-1: none).
-__device__ __forceinline__ int advance(const LaunchArgs &a, const View &v, Lane &L, uint16_t *cuts,
+__device__ __forceinline__ int advance(const WorkItem &a, const View &v, Lane &L, uint16_t *cuts,
                                        int cs) {
     const SubHdr *S = v.S;
     uint32_t c = 0;
@@ -350,7 +364,7 @@ __device__ uint32_t spatial_terms(const View &v, int32_t Ls, const int32_t split
 }
 
 template <int FAM>
-__device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid &m) {
+__device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid &m, const HaloEntry *halo = nullptr) {
     const ImgHdr *H = v.H;
     const SubHdr *S = v.S;
     const ModelHdr *M = v.M;
@@ -386,7 +400,14 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.comp = comp_term(B * M->FB, M->WU, p, 1, tau);
         const int32_t Ls = at<int32_t>(v.img, S->off_Ls)[L.d[D_LS]];
         int64_t NS, HV;
-        reason |= spatial_terms(v, Ls, split, NS, HV);
+        if (halo) {
+            const HaloEntry &he = halo[L.d[D_DIMS] * S->radix[D_LS] + L.d[D_LS]];
+            NS = he.NS;
+            HV = he.HV;
+            reason |= he.reason;
+        } else {
+            reason |= spatial_terms(v, Ls, split, NS, HV);
+        }
         const int ti = tier_of(H, p2), to = tier_of(H, p);
         reason |= flag_tier(ti) | flag_tier(to);
         m.h_on = p2 > 1;
@@ -474,11 +495,11 @@ struct Phases {
 
 // alpha/beta-dependent part and the t_iter fold ((((comp+GE)+AG)+AR)+Halo)+P2P.
 // EXPLAIN: also report phases, with +inf for a phase whose tier is missing.
-template <int FAM, bool EXPLAIN>
+template <int FAM, bool EXPLAIN, bool CHECK_TIER = true>
 __device__ __forceinline__ double inner(const Mid &m, const double *arow, const double *brow, Phases *ph) {
     double ge = 0.0, ag = 0.0, ar = 0.0, halo = 0.0, p2p = 0.0;
     double t = m.comp;
-    if (!EXPLAIN && (m.reason & PARADL_R_TIER)) return CUDART_INF;
+    if (!EXPLAIN && CHECK_TIER && (m.reason & PARADL_R_TIER)) return CUDART_INF;
     auto ar_eval = [&](const ARt &r, double phi, bool use_phi) -> double {
         if (!r.on) return 0.0;
         if (EXPLAIN && r.t < 0) return CUDART_INF;
@@ -535,6 +556,81 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
         ph->p2p = p2p;
     }
     return t;
+}
+
+// Branch-free form of inner() for the sweep's hot loop: absent phases carry zero
+// coefficients (t + 0*x == t exactly for finite x), tiers are clamped to a valid row.
+// Only used where no tier is missing (reduce mode evaluates feasible configs only;
+// dense mode checks PARADL_R_TIER first), so results equal inner() bit for bit.
+__device__ __forceinline__ void fastify(Mid &m) {
+    if (!m.ge.on) m.ge.c = m.ge.s = 0.0;
+    if (!m.ge2.on) m.ge2.c = m.ge2.s = 0.0;
+    if (!m.ag_on) m.ag_c = m.ag_na = m.ag_s = 0.0;
+    if (!m.h_on) m.h_na = m.h_s = 0.0;
+    if (!m.pp_on) m.pp_c = m.pp_na = m.pp_s = 0.0;
+    m.ge.t = max(m.ge.t, 0);
+    m.ge2.t = max(m.ge2.t, 0);
+    m.ag_t = max(m.ag_t, 0);
+    m.h_t = max(m.h_t, 0);
+    m.pp_t = max(m.pp_t, 0);
+}
+
+// The alpha/beta-dependent part split into alpha-derived values (one alpha row), beta-slot
+// values (products s*beta, invariant over alpha) and their combination.  The operations
+// and their order are exactly those of inner(); splitting only decides which results are
+// computed once and reused.
+struct AlphaV {
+    double ge, ge2, ag, h, pp;
+};
+struct SlotV {
+    double ge, ge2, ag, h, pp;
+};
+
+template <int FAM>
+__device__ __forceinline__ void alpha_vals(const Mid &m, const double *arow, AlphaV &a) {
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_DF)
+        a.ge = arow[m.ge.t];
+    if (FAM == PARADL_DS) a.ge2 = arow[m.ge2.t];
+    if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) a.ag = dmul(m.ag_na, arow[m.ag_t]);
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) a.h = dmul(m.h_na, arow[m.h_t]);
+    if (FAM == PARADL_PIPELINE || FAM == PARADL_PD) a.pp = arow[m.pp_t];
+    if (FAM == PARADL_LAYERPURE) a.pp = dmul(m.pp_na, arow[m.pp_t]);
+}
+
+template <int FAM>
+__device__ __forceinline__ void slot_vals(const Mid &m, const double *brow, SlotV &v) {
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS)
+        v.ge = dmul(m.ge.s, brow[m.ge.t]);
+    if (FAM == PARADL_DF) v.ge = dmul(m.ge.s, dmul(brow[m.ge.t], m.phi));
+    if (FAM == PARADL_DS) v.ge2 = dmul(m.ge2.s, brow[m.ge2.t]);
+    if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) v.ag = dmul(m.ag_s, brow[m.ag_t]);
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) v.h = dmul(m.h_s, brow[m.h_t]);
+    if (FAM == PARADL_PIPELINE || FAM == PARADL_PD || FAM == PARADL_LAYERPURE) v.pp = dmul(m.pp_s, brow[m.pp_t]);
+}
+
+template <int FAM>
+__device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const SlotV &v) {
+    double t = m.comp;
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DF)
+        t = dadd(t, dmul(m.ge.c, dadd(a.ge, v.ge)));
+    if (FAM == PARADL_DS) t = dadd(t, dadd(dmul(m.ge.c, dadd(a.ge, v.ge)), dmul(m.ge2.c, dadd(a.ge2, v.ge2))));
+    if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) {
+        const double ag = dmul(m.ag_c, dadd(a.ag, v.ag));
+        t = dadd(dadd(t, ag), dmul(2.0, ag));
+    }
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) t = dadd(t, dmul(2.0, dadd(a.h, v.h)));
+    if (FAM == PARADL_PIPELINE || FAM == PARADL_PD) t = dadd(t, dmul(m.pp_c, dadd(a.pp, v.pp)));
+    if (FAM == PARADL_LAYERPURE) t = dadd(t, dmul(2.0, dadd(a.pp, v.pp)));
+    return t;
+}
+
+template <int FAM>
+__device__ __forceinline__ double inner_fast(const Mid &m, const double *arow, const double *brow) {
+    AlphaV a;
+    SlotV v;
+    alpha_vals<FAM>(m, arow, a);
+    slot_vals<FAM>(m, brow, v);
+    return combine<FAM>(m, a, v);
 }
 
 // ------------------------------------------------------------------ a8: warp top-k
@@ -595,11 +691,76 @@ struct WarpTopK {
             thi = tib;
         }
     }
+    // compare-exchange with lane^j: keep the smaller (keep_min) or the larger entry
+    __device__ __forceinline__ static void cx(double &k, uint64_t &i, int j, bool keep_min) {
+        const double ok = __shfl_xor_sync(0xffffffffu, k, j);
+        const uint64_t oi = __shfl_xor_sync(0xffffffffu, i, j);
+        const bool other_less = hit_less(ok, oi, k, i);
+        if (keep_min == other_less) {
+            k = ok;
+            i = oi;
+        }
+    }
+    // ascending bitonic sort of one entry per lane
+    __device__ __forceinline__ static void sort32(double &k, uint64_t &i) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int s = 2; s <= 32; s <<= 1)
+#pragma unroll
+            for (int j = s >> 1; j > 0; j >>= 1) cx(k, i, j, ((lane & s) == 0) == ((lane & j) == 0));
+    }
+    // ascending sort of a bitonic sequence held one entry per lane
+    __device__ __forceinline__ static void merge32(double &k, uint64_t &i) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) cx(k, i, j, (lane & j) == 0);
+    }
+    // batch insertion of up to 32 candidates (sentinels elsewhere): the 64 smallest of
+    // list(a,b) + C are a + the 32 smallest of b + C (every a <= every b)
+    __device__ void batch(double ck, uint64_t ci) {
+        const int lane = threadIdx.x & 31;
+        const unsigned full = 0xffffffffu;
+        sort32(ck, ci);
+        const double rk = __shfl_sync(full, ck, 31 - lane);
+        const uint64_t ri = __shfl_sync(full, ci, 31 - lane);
+        if (hit_less(rk, ri, kb, ib)) {
+            kb = rk;
+            ib = ri;
+        }
+        merge32(kb, ib);
+        const double bk = __shfl_sync(full, kb, 31 - lane);
+        const uint64_t bi = __shfl_sync(full, ib, 31 - lane);
+        if (hit_less(bk, bi, ka, ia)) {   // lower half keeps the min, upper half the max
+            kb = ka;
+            ib = ia;
+            ka = bk;
+            ia = bi;
+        } else {
+            kb = bk;
+            ib = bi;
+        }
+        merge32(ka, ia);
+        merge32(kb, ib);
+        const int src = (k - 1) & 31;
+        const double tka = __shfl_sync(full, ka, src), tkb = __shfl_sync(full, kb, src);
+        const uint64_t tia = __shfl_sync(full, ia, src), tib = __shfl_sync(full, ib, src);
+        if (k - 1 < 32) {
+            thk = tka;
+            thi = tia;
+        } else {
+            thk = tkb;
+            thi = tib;
+        }
+    }
     // whole warp; per-lane candidate (valid, key, idx)
     __device__ __forceinline__ void offer(bool valid, double key, uint64_t idx) {
         const unsigned full = 0xffffffffu;
         bool cand = valid && key <= thk && (key < thk || idx < thi);
         unsigned msk = __ballot_sync(full, cand);
+        if (__popc(msk) >= 6) {
+            batch(cand ? key : CUDART_INF, cand ? idx : ~0ull);
+            return;
+        }
         while (msk) {
             const int src = __ffs(msk) - 1;
             msk &= msk - 1;
@@ -610,31 +771,292 @@ struct WarpTopK {
     }
 };
 
+// ------------------------------------------------------------------ beta-slot run (reduce mode)
+// Evaluates `run` consecutive lane steps inside one alpha/beta block when n_beta = 32*M:
+// lane step r visits beta = base + 32*slot, slot cycling 0..M-1, alpha advancing after
+// slot M-1.  idx0 = global index of the lane's first configuration of the run.  On exit
+// (alpha_i, beta_i) is the lane's last evaluated configuration.
+template <int FAM, int M>
+__device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const double *alpha_tab, const double *beta_tab,
+                                          int NT, uint32_t &alpha_i, uint32_t &beta_i, uint32_t run, uint64_t idx0) {
+    const unsigned full = 0xffffffffu;
+    const uint32_t base = beta_i & 31u;
+    SlotV sv[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) slot_vals<FAM>(m, beta_tab + (size_t)(base + 32u * i) * NT, sv[i]);
+    uint32_t slot = beta_i >> 5;
+    uint32_t r = 0;
+    uint32_t a = alpha_i;
+    uint32_t last_a = a, last_slot = slot;
+    // phase: finish a partially visited alpha row (M == 2, starting at slot 1)
+    if (M == 2 && slot == 1) {
+        AlphaV av;
+        alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
+        const double key = dmul(combine<FAM>(m, av, sv[M - 1]), m.I);
+        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, idx0);
+        last_a = a;
+        last_slot = 1;
+        r = 1;
+        a++;
+    }
+    // whole alpha rows
+    while (r + M <= run) {
+        AlphaV av;
+        alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
+        double key[M];
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+            key[i] = dmul(combine<FAM>(m, av, sv[i]), m.I);
+            any |= key[i] <= tk.thk;
+        }
+        if (__any_sync(full, any)) {
+#pragma unroll
+            for (int i = 0; i < M; i++) tk.offer(true, key[i], idx0 + 32ull * (r + i));
+        }
+        last_a = a;
+        last_slot = M - 1;
+        r += M;
+        a++;
+    }
+    // tail (M == 2 only): slot 0 of one more row
+    if (r < run) {
+        AlphaV av;
+        alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
+        const double key = dmul(combine<FAM>(m, av, sv[0]), m.I);
+        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, idx0 + 32ull * r);
+        last_a = a;
+        last_slot = 0;
+    }
+    alpha_i = last_a;
+    beta_i = base + 32u * last_slot;
+}
+
 // ------------------------------------------------------------------ the sweep kernel
+// Block-wide ascending bitonic sort of n (power of two) hits by (key, idx) in shared memory.
+__device__ void bitonic_sort_smem(paradl_hit *x, int n) {
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const paradl_hit p = x[i], q = x[ixj];
+                    const bool up = (i & k) == 0;
+                    const bool gt = hit_less(q.key_epoch_s, q.idx, p.key_epoch_s, p.idx);
+                    if (gt == up) {
+                        x[i] = q;
+                        x[ixj] = p;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 struct SmemExtra {
     uint16_t cuts[kMaxCuts][kThreads];
     paradl_hit lists[kWarps][PARADL_MAX_TOPK];
 };
 
+// One tile (32*steps consecutive configurations of work item w) for the whole warp.
 template <int FAM, bool DENSE>
-__global__ void __launch_bounds__(kThreads) sweep_kernel(const LaunchArgs a) {
+__device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                                          uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt) {
+    const View v = make_view(smem, w.sub);
+    const int lane = threadIdx.x & 31;
+    const int cs = kThreads;
+    const int NT = v.H->n_tiers;
+    const double *alpha_tab = at<double>(v.img, v.S->off_alpha);
+    const double *beta_tab = at<double>(v.img, v.S->off_beta);
+    const uint64_t gbase = v.S->offset;   // global index of local index 0
+    const uint64_t TS = 32ull * w.steps;
+    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
+    const uint32_t nB = v.S->radix[D_BETA];
+    const uint32_t nAB = v.S->radix[D_ALPHA] * nB;     // host guarantees < 2^31
+    const uint32_t dB = 32u % nB, dA = 32u / nB;        // lane stride 32 inside the alpha/beta block
+    const bool slots = (nB == 32u || nB == 64u);        // beta-slot caching applies (M = nB / 32)
+    const bool M2 = nB == 64u;
+    const unsigned full = 0xffffffffu;
+        const uint64_t u0 = w.lo + tile * TS;
+        const uint64_t uend = (u0 + TS < w.hi) ? u0 + TS : w.hi;
+        const uint32_t len = (uint32_t)(uend - u0);       // <= 32 * steps
+        const uint32_t nsteps = (len + 31) >> 5;
+        const uint32_t nfull = len >> 5;                  // steps with all 32 lanes active
+        const uint64_t g0 = gbase + u0;                   // global index of the tile's first config
+
+        Lane L;
+        StageT st;
+        Mid m;
+        if ((uint32_t)lane < len) {
+            decode(v, u0 + lane, L, cuts, cs);
+            if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+            compute_mid<FAM>(v, L, st, m, w.halo);
+            fastify(m);
+        } else {
+            L.d[D_ALPHA] = L.d[D_BETA] = 0;
+            m.reason = PARADL_R_SCALING;
+        }
+        uint32_t alpha_i = L.d[D_ALPHA], beta_i = L.d[D_BETA];
+        uint32_t carry = 0;
+        bool have_carry = false;
+
+        // emits one step (step index jj within the tile) for every lane
+        auto emit_dense = [&](bool act, double t_it, bool feas, uint32_t jj) {
+            const uint64_t o = g0 + lane + 32ull * jj - a.first;
+            if (act) {
+                if (a.t_iter) a.t_iter[o] = t_it;
+                if (a.mem) a.mem[o] = m.mem;
+                if (a.reason) a.reason[o] = (uint8_t)m.reason;
+            }
+            if (a.bits) {
+                const unsigned bits = __ballot_sync(full, act && feas);
+                if (lane == 0) {
+                    const uint64_t pos0 = g0 + 32ull * jj - a.first;   // bit position of lane 0
+                    const uint32_t sh = (uint32_t)(pos0 & 31);
+                    const uint64_t w = pos0 >> 5;
+                    const uint32_t lo = bits << sh;
+                    const uint32_t hi = sh ? (bits >> (32 - sh)) : 0u;
+                    const uint32_t word = lo | (have_carry ? carry : 0u);
+                    const uint64_t wg0 = a.first + (w << 5);
+                    const bool excl = have_carry || sh == 0;
+                    const bool inside = wg0 >= g0 && wg0 + 32 <= gbase + uend;
+                    if (excl && inside) a.bits[w] = word;
+                    else if (word) atomicOr(&a.bits[w], word);
+                    carry = hi;
+                    have_carry = sh != 0;
+                }
+            }
+        };
+
+        uint32_t j = 0;
+        while (j < nsteps) {
+            if (j >= nfull) {
+                // ragged last step of the range: generic evaluation with an activity mask
+                const bool act = (uint32_t)lane + 32u * j < len;
+                const double *arow = alpha_tab + (size_t)alpha_i * NT;
+                const double *brow = beta_tab + (size_t)beta_i * NT;
+                const bool feas = act && m.reason == 0;
+                if (DENSE) {
+                    const double t_it = (act && !(m.reason & PARADL_R_TIER)) ? inner_fast<FAM>(m, arow, brow) : CUDART_INF;
+                    emit_dense(act, t_it, feas, j);
+                } else {
+                    const double key = feas ? dmul(inner_fast<FAM>(m, arow, brow), m.I) : CUDART_INF;
+                    cnt += feas ? 1u : 0u;
+                    tk.offer(feas, key, g0 + lane + 32ull * j);
+                }
+                j++;
+                break;
+            }
+            // a run: consecutive steps in which no lane leaves its alpha/beta block
+            const uint32_t ab = alpha_i * nB + beta_i;
+            uint32_t run = __reduce_min_sync(full, (nAB - ab + 31u) >> 5);
+            run = min(run, nfull - j);
+            const bool feas = m.reason == 0;
+            if (!DENSE) {
+                const unsigned fb = __ballot_sync(full, feas);
+                if (fb == 0u) {
+                    if (run > 1) {   // no feasible lane: skip the run, closed-form advance
+                        const uint32_t nab = ab + 32u * (run - 1);
+                        alpha_i = nab / nB;
+                        beta_i = nab - alpha_i * nB;
+                    }
+                } else if (fb == full && slots) {
+                    // every lane feasible and n_beta = 32*M: lane's beta values are fixed, so the
+                    // s*beta products are formed once per run and reused for every alpha row
+                    if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                    else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                } else if (fb == full) {
+                    // every lane feasible: branch-free evaluation, rare slow path for insertions
+#pragma unroll 2
+                    for (uint32_t r = 0; r < run; r++) {
+                        const double key = dmul(inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
+                                                                beta_tab + (size_t)beta_i * NT),
+                                                m.I);
+                        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
+                        beta_i += dB;
+                        alpha_i += dA;
+                        if (beta_i >= nB) {
+                            beta_i -= nB;
+                            alpha_i++;
+                        }
+                    }
+                    // undo the advance after the run's last step (the generic odometer takes it)
+                    {
+                        const uint32_t nab = ab + 32u * (run - 1);
+                        alpha_i = nab / nB;
+                        beta_i = nab - alpha_i * nB;
+                    }
+                } else {
+                    for (uint32_t r = 0; r < run; r++) {
+                        double key = CUDART_INF;
+                        if (feas)
+                            key = dmul(inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
+                                                       beta_tab + (size_t)beta_i * NT),
+                                       m.I);
+                        if (__any_sync(full, feas && key <= tk.thk)) tk.offer(feas, key, g0 + lane + 32ull * (j + r));
+                        if (r + 1 < run) {
+                            beta_i += dB;
+                            alpha_i += dA;
+                            if (beta_i >= nB) {
+                                beta_i -= nB;
+                                alpha_i++;
+                            }
+                        }
+                    }
+                }
+                cnt += feas ? run : 0u;
+            } else {
+                const bool tier_ok = !(m.reason & PARADL_R_TIER);
+                for (uint32_t r = 0; r < run; r++) {
+                    const double t_it = tier_ok ? inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
+                                                                  beta_tab + (size_t)beta_i * NT)
+                                                : CUDART_INF;
+                    emit_dense(true, t_it, feas, j + r);
+                    if (r + 1 < run) {
+                        beta_i += dB;
+                        alpha_i += dA;
+                        if (beta_i >= nB) {
+                            beta_i -= nB;
+                            alpha_i++;
+                        }
+                    }
+                }
+            }
+            j += run;
+            if (j < nsteps && (uint32_t)lane + 32u * j < len) {
+                // step into the next configuration: generic odometer (may leave the block)
+                L.d[D_ALPHA] = alpha_i;
+                L.d[D_BETA] = beta_i;
+                const int lvl = advance(w, v, L, cuts, cs);
+                if (lvl >= D_LS) {
+                    if (PIPE && lvl >= D_PART)
+                        stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+                    compute_mid<FAM>(v, L, st, m, w.halo);
+                    fastify(m);
+                }
+                alpha_i = L.d[D_ALPHA];
+                beta_i = L.d[D_BETA];
+            }
+        }
+        if (DENSE && a.bits && lane == 0 && have_carry && carry) {
+            const uint64_t pos_end = g0 + 32ull * nsteps - a.first;
+            atomicOr(&a.bits[pos_end >> 5], carry);
+        }
+    
+}
+
+template <int FAM, bool DENSE>
+__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ unsigned long long s_count;
     if (threadIdx.x == 0) s_count = 0;
     stage_image(smem, a.img, a.img_bytes, &mbar);
     SmemExtra *ex = reinterpret_cast<SmemExtra *>(smem + a.img_bytes);
-    const View v = make_view(smem, a.sub);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint16_t *cuts = &ex->cuts[0][threadIdx.x];
-    const int cs = kThreads;
-    const int NT = v.H->n_tiers;
-    const double *alpha_tab = at<double>(v.img, v.S->off_alpha);
-    const double *beta_tab = at<double>(v.img, v.S->off_beta);
-    const uint64_t gbase = v.S->offset;   // global index of local index 0
-    const uint64_t TS = 32ull * a.steps;
-    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
-
+    const unsigned full = 0xffffffffu;
     WarpTopK tk;
     tk.init(a.k);
     unsigned long long cnt = 0;
@@ -642,165 +1064,132 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const LaunchArgs a) {
     for (;;) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(a.tile_counter, 1ull);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        const uint64_t tile = t * (uint64_t)a.n_shards + (uint64_t)a.shard;
-        if (tile >= a.n_tiles) break;
-        const uint64_t u0 = a.lo + tile * TS;
-        const uint64_t uend = (u0 + TS < a.hi) ? u0 + TS : a.hi;
-
-        Lane L;
-        StageT st;
-        Mid m;
-        uint64_t u = u0 + lane;
-        bool active = u < uend;
-        if (active) {
-            decode(v, u, L, cuts, cs);
-            if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
-            compute_mid<FAM>(v, L, st, m);
-        }
-        uint32_t carry = 0;
-        uint64_t wlast = 0;
-        bool have_carry = false;
-        for (uint64_t s0 = u0; s0 < uend; s0 += 32) {
-            active = u < uend;
-            double key = CUDART_INF, t_it = CUDART_INF;
-            bool feas = false;
-            if (active) {
-                const double *arow = alpha_tab + (size_t)L.d[D_ALPHA] * NT;
-                const double *brow = beta_tab + (size_t)L.d[D_BETA] * NT;
-                if (DENSE || m.reason == 0) {
-                    t_it = inner<FAM, false>(m, arow, brow, nullptr);
-                    key = dmul(t_it, m.I);
-                }
-                feas = m.reason == 0;
-            }
-            const uint64_t gidx = gbase + u;
-            if (!DENSE) {
-                cnt += (active && feas) ? 1u : 0u;
-                tk.offer(active && feas, key, gidx);
-            } else {
-                const uint64_t o = gidx - a.first;
-                if (active) {
-                    if (a.t_iter) a.t_iter[o] = t_it;
-                    if (a.mem) a.mem[o] = m.mem;
-                    if (a.reason) a.reason[o] = (uint8_t)m.reason;
-                }
-                if (a.bits) {
-                    const unsigned bits = __ballot_sync(0xffffffffu, active && feas);
-                    if (lane == 0) {
-                        const uint64_t pos0 = gbase + s0 - a.first;   // bit position of this step's lane 0
-                        const uint32_t sh = (uint32_t)(pos0 & 31);
-                        const uint64_t w = pos0 >> 5;
-                        const uint32_t lo = bits << sh;
-                        const uint32_t hi = sh ? (bits >> (32 - sh)) : 0u;
-                        const uint32_t word = lo | (have_carry ? carry : 0u);
-                        // exclusive iff every bit of word w maps into this tile's range
-                        const uint64_t wg0 = a.first + (w << 5);
-                        const bool excl = have_carry || sh == 0;
-                        const bool inside = wg0 >= gbase + u0 && wg0 + 32 <= gbase + uend;
-                        if (excl && inside) a.bits[w] = word;
-                        else if (word) atomicOr(&a.bits[w], word);
-                        carry = hi;
-                        have_carry = sh != 0;
-                        wlast = w + 1;
-                    }
-                }
-            }
-            // advance every lane by 32 indices
-            u += 32;
-            if (u < uend) {
-                const int lvl = advance(a, v, L, cuts, cs);
-                if (lvl >= D_LS) {
-                    if (PIPE && lvl >= D_PART)
-                        stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
-                    compute_mid<FAM>(v, L, st, m);
-                }
-            }
-        }
-        if (DENSE && a.bits && lane == 0 && have_carry && carry) atomicOr(&a.bits[wlast], carry);
+        t = __shfl_sync(full, t, 0);
+        const uint64_t T = t * (uint64_t)a.n_shards + (uint64_t)a.shard;
+        if (T >= a.total_tiles) break;
+        int wi = 0;
+        while (wi + 1 < a.n_work && T >= a.work[wi + 1].tile_base) wi++;
+        const WorkItem &w = a.work[wi];
+        tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
     }
 
     if (!DENSE) {
-        // CTA merge: warps publish their lists; warp 0 inserts the others into its own.
-        paradl_hit *mine = ex->lists[warp];
-        mine[lane].idx = tk.ia;
-        mine[lane].key_epoch_s = tk.ka;
-        mine[lane + 32].idx = tk.ib;
-        mine[lane + 32].key_epoch_s = tk.kb;
+        // CTA merge: the 8 warp lists (512 entries) are bitonic-sorted in shared memory and
+        // the first k written out.
+        paradl_hit *lst = &ex->lists[0][0];
+        lst[warp * PARADL_MAX_TOPK + lane].idx = tk.ia;
+        lst[warp * PARADL_MAX_TOPK + lane].key_epoch_s = tk.ka;
+        lst[warp * PARADL_MAX_TOPK + lane + 32].idx = tk.ib;
+        lst[warp * PARADL_MAX_TOPK + lane + 32].key_epoch_s = tk.kb;
         atomicAdd(&s_count, cnt);
         __syncthreads();
-        if (warp == 0) {
-            for (int w = 1; w < kWarps; w++) {
-                for (int e = 0; e < a.k; e += 32) {
-                    const int j = e + lane;
-                    const bool ok = j < a.k;
-                    const double kk = ok ? ex->lists[w][j].key_epoch_s : CUDART_INF;
-                    const uint64_t ii = ok ? ex->lists[w][j].idx : ~0ull;
-                    tk.offer(ok && ii != ~0ull, kk, ii);
-                }
-            }
-            paradl_hit *out = a.cta_lists + (size_t)blockIdx.x * a.k;
-            if (lane < a.k) {
-                out[lane].idx = tk.ia;
-                out[lane].key_epoch_s = tk.ka;
-            }
-            if (lane + 32 < a.k) {
-                out[lane + 32].idx = tk.ib;
-                out[lane + 32].key_epoch_s = tk.kb;
-            }
-            if (lane == 0) atomicAdd(a.count, s_count);
-        }
+        bitonic_sort_smem(lst, kWarps * PARADL_MAX_TOPK);
+        paradl_hit *out = a.cta_lists + (size_t)blockIdx.x * a.k;
+        for (int i = threadIdx.x; i < a.k; i += blockDim.x) out[i] = lst[i];
+        if (threadIdx.x == 0) atomicAdd(a.count, s_count);
     }
 }
 
 // ------------------------------------------------------------------ merge kernel
-// Merges n_lists sorted-or-not lists of k hits and sums n_counts counts.
+// Merges n_lists ascending lists of k hits (as produced by the sweep kernels and by
+// paradl_topk_async) and sums n_counts counts.  The k-th entry of any full list bounds
+// the k-th global entry, so only entries <= the smallest such bound can survive: one
+// thread per list collects them (early exit, lists are sorted), then one warp selects.
+constexpr int kMergeCand = 2048;
+
+__device__ __forceinline__ void hit_min(double &k, uint64_t &i, double k2, uint64_t i2) {
+    if (hit_less(k2, i2, k, i)) {
+        k = k2;
+        i = i2;
+    }
+}
+
 __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, int64_t n_lists, int32_t k,
                                                       const unsigned long long *counts, int32_t n_counts,
                                                       paradl_hit *out, unsigned long long *count_out) {
-    __shared__ paradl_hit s_lists[32][PARADL_MAX_TOPK];
+    __shared__ paradl_hit cand[kMergeCand];
     __shared__ unsigned long long s_cnt;
+    __shared__ double s_wk[32];
+    __shared__ uint64_t s_wi[32];
+    __shared__ int s_nc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_cnt = 0;
+    const unsigned full = 0xffffffffu;
+    if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_nc = 0;
+    }
     __syncthreads();
     unsigned long long c = 0;
     for (int i = threadIdx.x; i < n_counts; i += blockDim.x) c += counts[i];
     atomicAdd(&s_cnt, c);
-    WarpTopK tk;
-    tk.init(k);
-    const int64_t n = n_lists * (int64_t)k;
-    const int nw = blockDim.x >> 5;
-    for (int64_t base = (int64_t)warp * 32; base < n; base += (int64_t)nw * 32) {
-        const int64_t j = base + lane;
-        const bool ok = j < n;
-        const double kk = ok ? lists[j].key_epoch_s : CUDART_INF;
-        const uint64_t ii = ok ? lists[j].idx : ~0ull;
-        tk.offer(ok && ii != ~0ull, kk, ii);
+    // 1. bound: smallest k-th entry over the lists
+    double bk = CUDART_INF;
+    uint64_t bi = ~0ull;
+    for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) hit_min(bk, bi, lists[l * k + (k - 1)].key_epoch_s, lists[l * k + (k - 1)].idx);
+    for (int o = 16; o; o >>= 1) hit_min(bk, bi, __shfl_xor_sync(full, bk, o), __shfl_xor_sync(full, bi, o));
+    if (lane == 0) {
+        s_wk[warp] = bk;
+        s_wi[warp] = bi;
     }
-    s_lists[warp][lane].idx = tk.ia;
-    s_lists[warp][lane].key_epoch_s = tk.ka;
-    s_lists[warp][lane + 32].idx = tk.ib;
-    s_lists[warp][lane + 32].key_epoch_s = tk.kb;
     __syncthreads();
     if (warp == 0) {
-        for (int w = 1; w < nw; w++)
-            for (int e = 0; e < k; e += 32) {
-                const int j = e + lane;
-                const bool ok = j < k;
-                const double kk = ok ? s_lists[w][j].key_epoch_s : CUDART_INF;
-                const uint64_t ii = ok ? s_lists[w][j].idx : ~0ull;
-                tk.offer(ok && ii != ~0ull, kk, ii);
-            }
-        if (lane < k) {
-            out[lane].idx = tk.ia;
-            out[lane].key_epoch_s = tk.ka;
+        bk = lane < (int)(blockDim.x >> 5) ? s_wk[lane] : CUDART_INF;
+        bi = lane < (int)(blockDim.x >> 5) ? s_wi[lane] : ~0ull;
+        for (int o = 16; o; o >>= 1) hit_min(bk, bi, __shfl_xor_sync(full, bk, o), __shfl_xor_sync(full, bi, o));
+        if (lane == 0) {
+            s_wk[0] = bk;
+            s_wi[0] = bi;
         }
-        if (lane + 32 < k) {
-            out[lane + 32].idx = tk.ib;
-            out[lane + 32].key_epoch_s = tk.kb;
-        }
-        if (lane == 0) *count_out = s_cnt;
     }
+    __syncthreads();
+    bk = s_wk[0];
+    bi = s_wi[0];
+    // 2. candidates <= bound (sorted lists: stop at the first larger entry)
+    for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
+        for (int j = 0; j < k; j++) {
+            const paradl_hit h = lists[l * k + j];
+            if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) break;
+            const int pos = atomicAdd(&s_nc, 1);
+            if (pos < kMergeCand) cand[pos] = h;
+        }
+    }
+    __syncthreads();
+    const int nc = s_nc;
+    if (nc <= kMergeCand) {
+        // sort the candidates (padded to a power of two) and keep the first k
+        int n2 = 64;   // >= k (k <= 64) so that out[] never reads unsorted slots
+        while (n2 < nc) n2 <<= 1;
+        for (int i = nc + threadIdx.x; i < n2; i += blockDim.x) {
+            cand[i].idx = ~0ull;
+            cand[i].key_epoch_s = CUDART_INF;
+        }
+        __syncthreads();
+        bitonic_sort_smem(cand, n2);
+        for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = cand[i];
+        if (threadIdx.x == 0) *count_out = s_cnt;
+        return;
+    }
+    if (warp != 0) return;
+    // pathological ties: one warp scans everything
+    WarpTopK tk;
+    tk.init(k);
+    {
+        const int64_t n = n_lists * (int64_t)k;
+        for (int64_t e = 0; e < n; e += 32) {
+            const int64_t j = e + lane;
+            const bool ok = j < n && lists[j].idx != ~0ull;
+            tk.offer(ok, ok ? lists[j].key_epoch_s : CUDART_INF, ok ? lists[j].idx : ~0ull);
+        }
+    }
+    if (lane < k) {
+        out[lane].idx = tk.ia;
+        out[lane].key_epoch_s = tk.ka;
+    }
+    if (lane + 32 < k) {
+        out[lane + 32].idx = tk.ib;
+        out[lane + 32].key_epoch_s = tk.kb;
+    }
+    if (lane == 0) *count_out = s_cnt;
 }
 
 // ------------------------------------------------------------------ explain / decode
@@ -961,6 +1350,73 @@ __global__ void prep_model_kernel(const paradl_layer *rows, int32_t G, int64_t D
     M->Cmin2 = Cmin2;
 }
 
+// ------------------------------------------------------------------ a5: halo table
+// One warp per (dims, Ls) entry of each spatial / ds sub-sweep of the launch: lanes split
+// the rows, then the integer halo volume / row count are summed and the split-limit bits
+// OR-ed across the warp -- the same quantities spatial_terms computes row by row.
+__global__ void halo_table_kernel(const __grid_constant__ HaloJobs J) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= J.total_entries) return;
+    int jb = 0;
+    while (jb + 1 < J.n_jobs && gw >= J.job[jb + 1].entry_base) jb++;
+    const HaloJob &job = J.job[jb];
+    const int e = gw - job.entry_base;
+    const View v = make_view(J.img, job.sub);
+    const uint32_t nL = v.S->radix[D_LS];
+    const uint32_t id = e / nL, il = e - id * nL;
+    const int32_t *dm = at<int32_t>(J.img, v.S->off_dims) + 4 * id;
+    const int32_t split[3] = {dm[1], dm[2], dm[3]};
+    const int32_t Ls = at<int32_t>(J.img, v.S->off_Ls)[il];
+    const RowGeo *geo = at<RowGeo>(v.mb, v.M->off_geo);
+    const int G = v.M->G;
+    const int lim = Ls < G ? Ls : G;
+    int64_t NS = 0, HV = 0;
+    uint32_t reason = 0;
+    for (int l = lane; l < lim; l += 32) {
+        const RowGeo &r = geo[l];
+        if (r.kind != PARADL_CONV && r.kind != PARADL_POOL) continue;
+        NS++;
+        for (int ax = 0; ax < 3; ax++) {
+            if (split[ax] <= 1) continue;
+            const int64_t h = r.K[ax] / 2;
+            if (split[ax] > r.X[ax]) reason |= PARADL_R_SCALING;
+            if (ceil_div64(r.X[ax], split[ax]) < h || ceil_div64(r.Y[ax], split[ax]) < h) reason |= PARADL_R_SPLIT;
+            if (h == 0) continue;
+            const int64_t nnb = split[ax] > 2 ? 2 : 1;
+            int64_t cx = 1, cy = 1;
+            for (int o = 0; o < 3; o++) {
+                if (o == ax) continue;
+                cx *= ceil_div64(r.X[o], split[o]);
+                cy *= ceil_div64(r.Y[o], split[o]);
+            }
+            HV += (int64_t)r.C * h * cx * nnb + (int64_t)r.F * h * cy * nnb;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        NS += __shfl_xor_sync(0xffffffffu, NS, o);
+        HV += __shfl_xor_sync(0xffffffffu, HV, o);
+        reason |= __shfl_xor_sync(0xffffffffu, reason, o);
+    }
+    if (lane == 0) {
+        HaloEntry hh;
+        hh.NS = NS;
+        hh.HV = HV;
+        hh.reason = reason;
+        hh.pad0 = 0;
+        hh.pad1 = 0;
+        job.tab[e] = hh;
+    }
+}
+
+cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st) {
+    const int threads = 256;
+    const long long warps = jobs.total_entries;
+    const int blocks = (int)((warps * 32 + threads - 1) / threads);
+    void *args[] = {const_cast<HaloJobs *>(&jobs)};
+    return cudaLaunchKernel((void *)halo_table_kernel, dim3(blocks), dim3(threads), args, 0, st);
+}
+
 // ------------------------------------------------------------------ FP64 peak microbenchmark
 // 8 independent DFMA chains per thread; counts executed DFMA instructions.
 __global__ void __launch_bounds__(256) fp64_bench_kernel(int iters, double *sink) {
@@ -992,15 +1448,11 @@ cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t 
 }
 
 // ------------------------------------------------------------------ launchers
-template <int FAM, bool DENSE>
-static void *kernel_ptr() {
-    return (void *)sweep_kernel<FAM, DENSE>;
-}
+size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
 static void *sweep_fn(int family, bool dense) {
-#define PARADL_CASE(F)                                                              \
-    case F:                                                                         \
-        return dense ? kernel_ptr<F, true>() : kernel_ptr<F, false>();
+#define PARADL_CASE(F) \
+    case F: return dense ? (void *)sweep_kernel<F, true> : (void *)sweep_kernel<F, false>;
     switch (family) {
         PARADL_CASE(PARADL_SERIAL)
         PARADL_CASE(PARADL_DATA)
@@ -1016,8 +1468,6 @@ static void *sweep_fn(int family, bool dense) {
     }
 #undef PARADL_CASE
 }
-
-size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
 int max_blocks_per_sm(int family, bool dense, size_t smem) {
     void *fn = sweep_fn(family, dense);

@@ -68,40 +68,68 @@ struct SubHdr {
 };
 static_assert(sizeof(SubHdr) % 16 == 0, "SubHdr alignment");
 
-// Arguments of one sweep-kernel launch (one sub-sweep, a local index range).
+// Halo-table entry per (dims index, Ls index) of a spatial / ds sub-sweep (row a5).
+struct HaloEntry {
+    int64_t NS, HV;
+    uint32_t reason, pad0;
+    uint64_t pad1;
+};
+static_assert(sizeof(HaloEntry) == 32, "HaloEntry layout");
+
+// One contiguous local index range [lo, hi) of one sub-sweep inside a sweep launch.
+// Tiles of 32*steps consecutive configurations; tile_base = index of its first tile in
+// the launch's global tile space (all work items concatenated, spec order).
+struct WorkItem {
+    int32_t sub, family;
+    uint32_t steps;
+    int32_t inc_top;               // highest digit with a non-zero stride increment
+    uint64_t lo, hi, n_tiles, tile_base;
+    uint32_t inc[kDigits];         // mixed-radix digits of the lane stride 32
+    uint32_t pad;
+    uint64_t inc_part;
+    const HaloEntry *halo;         // spatial / ds: [n_dims][n_Ls] table (device global), else null
+};
+
+// Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
 struct LaunchArgs {
     const uint8_t *img;            // device image
     uint32_t img_bytes;            // multiple of 16
-    int32_t sub;
-    uint64_t lo, hi;               // local index range [lo, hi) within the sub-sweep
+    int32_t n_work;
     uint64_t first;                // global index of dense element 0
-    uint64_t n_tiles;
-    uint32_t steps;                // tile = 32 * steps consecutive indices
+    uint64_t total_tiles;
     int32_t shard, n_shards;
     unsigned long long *tile_counter;
-    int32_t k;
+    int32_t k, pad;
     paradl_hit *cta_lists;         // [gridDim.x][k] (reduce mode)
     unsigned long long *count;     // feasible count accumulator (reduce mode)
     double *t_iter;                // dense outputs (indexed by global idx - first)
     double *mem;
     uint32_t *bits;
     uint8_t *reason;
-    uint32_t inc[kDigits];         // mixed-radix digits of the lane stride 32
-    uint64_t inc_part;
-    int32_t inc_top;               // highest digit with a non-zero increment
-    uint64_t g_range_lo, g_range_hi; // global [first, first+count) (dense bit ownership)
+    WorkItem work[kMaxSub];
+};
+
+struct HaloJob {
+    int32_t sub, n_entries;
+    int32_t entry_base, pad;
+    HaloEntry *tab;
+};
+struct HaloJobs {
+    const uint8_t *img;
+    int32_t n_jobs, total_entries;
+    HaloJob job[kMaxSub];
 };
 
 // launchers implemented in kernels.cu
 cudaError_t launch_prep_model(const paradl_layer *d_rows, int32_t G, int64_t D, uint8_t *d_block,
                               const ModelHdr &layout, cudaStream_t st);
-cudaError_t launch_sweep(int family, bool dense, const LaunchArgs &a, int grid, size_t smem,
-                         cudaStream_t st);
+cudaError_t launch_sweep(int family, bool dense, const LaunchArgs &a, int grid, size_t smem, cudaStream_t st);
 int max_blocks_per_sm(int family, bool dense, size_t smem);
 size_t sweep_smem_extra();
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
                          unsigned long long *count_out, cudaStream_t st);
+cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
 cudaError_t launch_explain(const uint8_t *img, uint32_t img_bytes, int32_t sub, uint64_t local,
                            paradl_config *d_cfg, paradl_prediction *d_pred, cudaStream_t st);
