@@ -30,11 +30,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 K_TOP = 64
-# FP64-pipe instructions per configuration in the inner (alpha/beta) loop of the
-# dominant kernel, counted from the canonical tree: pipeline family:
-# s*beta, alpha+, c*, comp+, *I, compare  = 6
-FP64_OPS_PER_CONFIG = {"pipeline": 6, "data": 6, "filter": 9, "channel": 9, "spatial": 11, "df": 14,
-                       "ds": 15, "pd": 10, "layerpure": 7, "serial": 3}
+# Algorithmic FP64-pipe instructions per configuration: the alpha/beta-dependent increment of
+# the canonical tree, after hoisting what is invariant over the inner radices
+# (s*beta is alpha-invariant).  Pipeline family: (alpha + s*beta), c*( ), comp + ( ), *I,
+# and the top-k admission compare = 5.
+FP64_OPS_PER_CONFIG = {"pipeline": 5, "data": 5, "filter": 7, "channel": 7, "spatial": 8, "df": 10,
+                       "ds": 11, "pd": 8, "layerpure": 5, "serial": 3}
 
 
 def parse():
@@ -146,7 +147,7 @@ def reference_arm(args):
             "unit": "configs/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
             "config": {"workload": sweep.name}}
-    per_step_s = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_s = max(0.3, min(5.0, 120.0 / max(1, args.steps + args.warmup)))
     from oracle import oracle as O
     osw = O.OracleSweep(sweep)
     n = osw.size()
@@ -208,16 +209,15 @@ def ours(args):
 
     launches = [0]
 
+    from paper_2104_09075_b200 import dist as PD
+
     def step():
-        ctx.topk_async(spec, 0, N, rank, ws, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
-        launches[0] += ctx.stat(2)
         if ws > 1:
-            dist.all_gather_into_tensor(lists.view(ws, -1), my_hits.view(-1))
-            dist.all_gather_into_tensor(counts, my_cnt)
-            ctx.merge_topk(lists.data_ptr(), ws, K_TOP, counts.data_ptr(), out.data_ptr(), out_cnt.data_ptr(),
-                           stream=stream)
-            launches[0] += 1
+            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_hits, my_cnt, stream=stream)
+            launches[0] += st_["launches"]
             return out, out_cnt
+        ctx.topk_async(spec, 0, N, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        launches[0] += ctx.stat(2)
         return my_hits, my_cnt
 
     for _ in range(args.warmup):
@@ -276,12 +276,8 @@ def ours(args):
             dist.barrier()
             t0 = time.perf_counter()
             ctx.set_system(sweep.system)
-            ctx.topk_async(spec, 0, N, rank, ws, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
-            h2d = ctx.stat(0)
-            dist.all_gather_into_tensor(lists.view(ws, -1), my_hits.view(-1))
-            dist.all_gather_into_tensor(counts, my_cnt)
-            ctx.merge_topk(lists.data_ptr(), ws, K_TOP, counts.data_ptr(), out.data_ptr(), out_cnt.data_ptr(),
-                           stream=stream)
+            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_hits, my_cnt, stream=stream)
+            h2d = st_["h2d"]
             host = out.cpu()
             _ = out_cnt.cpu()
             d2h = host.numel() * 8 + 8

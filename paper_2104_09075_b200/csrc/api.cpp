@@ -635,10 +635,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         grids[li] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid_max, need_ctas));
         total_ctas += grids[li];
     }
-    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 1)));
+    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 2)));
     if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * total_ctas * k));
     unsigned long long *ctr = (unsigned long long *)c->counters.p;
     CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
+    CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
     if (halo_entries) {
         CUDA_TRY(c, launch_halo_tables(hj, st));
         c->stat_launches++;
@@ -667,6 +668,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         a.n_shards = n_shards;
         a.tile_counter = ctr + li;
         a.count = ctr + nl;
+        a.gbound = ctr + nl + 1;
         a.k = k;
         a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
         if (dense) {

@@ -315,17 +315,31 @@ struct Mid {
     double pp_c, pp_na, pp_s;
     int pp_t;
     bool pp_on;           // pipeline c (alpha + s beta) / layer-pure 2 (na alpha + s beta)
+    // memoised divisions (same operands -> same IEEE result; recomputed when an operand changes)
+    double R_memo, tau_memo;
+    int64_t B_memo;
+    double I_memo;
+    int64_t bS_b, bS_S;
+    double bS_memo;
+    __device__ void reset_memo() {
+        R_memo = -1.0;
+        B_memo = -1;
+        bS_b = bS_S = -1;
+    }
 };
 
 // comp row of Table 2: ((B FB)/p_c) tau + (WU/p_u) tau
+// x / 1.0 == x exactly, so a division by 1 is skipped
+__device__ __forceinline__ double div_i(int64_t num, int64_t den) {
+    return den == 1 ? i2d(num) : ddiv(i2d(num), i2d(den));
+}
 __device__ __forceinline__ double comp_term(int64_t BFB, int64_t WU, int64_t pc, int64_t pu, double tau) {
-    return dadd(dmul(ddiv(i2d(BFB), i2d(pc)), tau), dmul(ddiv(i2d(WU), i2d(pu)), tau));
+    return dadd(dmul(div_i(BFB, pc), tau), dmul(div_i(WU, pu), tau));
 }
 // mem row of Table 2: gamma (delta ((2B XY)/p_a + (2W)/p_w + BI))
 __device__ __forceinline__ double mem_term(const ImgHdr *H, int64_t twoBXY, int64_t W, int64_t BI,
                                            int64_t pa, int64_t pw) {
-    return dmul(H->gamma, dmul(i2d(H->delta), dadd(dadd(ddiv(i2d(twoBXY), i2d(pa)), ddiv(i2d(2 * W), i2d(pw))),
-                                                   i2d(BI))));
+    return dmul(H->gamma, dmul(i2d(H->delta), dadd(dadd(div_i(twoBXY, pa), div_i(2 * W, pw)), i2d(BI))));
 }
 
 __device__ __forceinline__ uint32_t flag_tier(int t) { return t < 0 ? (uint32_t)PARADL_R_TIER : 0u; }
@@ -370,7 +384,11 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
     const ModelHdr *M = v.M;
     const double cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
     const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
-    const double tau = ddiv(1.0, R);
+    if (R != m.R_memo) {
+        m.R_memo = R;
+        m.tau_memo = ddiv(1.0, R);
+    }
+    const double tau = m.tau_memo;
     const int64_t b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
     const int32_t *dm = at<int32_t>(v.img, S->off_dims) + 4 * L.d[D_DIMS];
     const int64_t delta = H->delta;
@@ -465,7 +483,12 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.pp_s = i2d(delta * b * st.sumY);
             m.pp_t = ts;
         } else {
-            const double bS = ddiv(i2d(b), i2d(Sg));
+            if (b != m.bS_b || Sg != m.bS_S) {
+                m.bS_b = b;
+                m.bS_S = Sg;
+                m.bS_memo = ddiv(i2d(b), i2d(Sg));
+            }
+            const double bS = m.bS_memo;
             const double cseg = dmul(i2d(ns + Sg - 1), bS);
             m.comp = dadd(dmul(dmul(cseg, i2d(st.maxF + st.maxB)), tau), dmul(i2d(st.maxU), tau));
             m.pp_on = ns > 1;
@@ -482,7 +505,11 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
         if (Sg < 1 || Sg > b) reason |= PARADL_R_SEGMENTS;
     }
-    m.I = ddiv(i2d(M->D), i2d(B));   // Table 1: I = D/B
+    if (B != m.B_memo) {
+        m.B_memo = B;
+        m.I_memo = ddiv(i2d(M->D), i2d(B));   // Table 1: I = D/B
+    }
+    m.I = m.I_memo;
     if (!(m.mem <= cap)) reason |= PARADL_R_MEMORY;
     m.reason = reason;
     m.B = B;
@@ -644,11 +671,32 @@ struct WarpTopK {
     double ka, kb, thk;
     uint64_t ia, ib, thi;
     int k;
+    // Admission bound shared by every warp of the call: the k-th key of ANY full warp list
+    // bounds the global k-th key (that warp alone holds k entries <= it), so configs with a
+    // larger key can never enter the global top-k.  Kept as the bit pattern of a
+    // non-negative double (monotone as uint64) under atomicMin; ~0 = none yet.
+    double adm;
+    unsigned long long *gbound;
 
-    __device__ void init(int kk) {
+    __device__ void init(int kk, unsigned long long *g = nullptr) {
         k = kk;
-        ka = kb = thk = CUDART_INF;
+        ka = kb = thk = adm = CUDART_INF;
         ia = ib = thi = ~0ull;
+        gbound = g;
+    }
+    // re-read the shared bound (whole warp; cheap broadcast load)
+    __device__ __forceinline__ void refresh() {
+        if (!gbound) return;
+        const unsigned long long g = *(volatile unsigned long long *)gbound;
+        if (g != ~0ull) adm = fmin(thk, __longlong_as_double((long long)g));
+    }
+    // after thk changed: tighten adm and publish a full list's threshold
+    __device__ __forceinline__ void publish() {
+        if (thk < adm) {
+            adm = thk;
+            if (gbound && thk < CUDART_INF && (threadIdx.x & 31) == 0)
+                atomicMin(gbound, (unsigned long long)__double_as_longlong(thk));
+        }
     }
     // whole warp, uniform (key, idx)
     __device__ void insert(double key, uint64_t idx) {
@@ -690,6 +738,7 @@ struct WarpTopK {
             thk = tkb;
             thi = tib;
         }
+        publish();
     }
     // compare-exchange with lane^j: keep the smaller (keep_min) or the larger entry
     __device__ __forceinline__ static void cx(double &k, uint64_t &i, int j, bool keep_min) {
@@ -751,11 +800,12 @@ struct WarpTopK {
             thk = tkb;
             thi = tib;
         }
+        publish();
     }
     // whole warp; per-lane candidate (valid, key, idx)
     __device__ __forceinline__ void offer(bool valid, double key, uint64_t idx) {
         const unsigned full = 0xffffffffu;
-        bool cand = valid && key <= thk && (key < thk || idx < thi);
+        bool cand = valid && key <= adm && key <= thk && (key < thk || idx < thi);
         unsigned msk = __ballot_sync(full, cand);
         if (__popc(msk) >= 6) {
             batch(cand ? key : CUDART_INF, cand ? idx : ~0ull);
@@ -793,24 +843,51 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
         AlphaV av;
         alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
         const double key = dmul(combine<FAM>(m, av, sv[M - 1]), m.I);
-        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, idx0);
+        if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, idx0);
         last_a = a;
         last_slot = 1;
         r = 1;
         a++;
     }
-    // whole alpha rows
+    // R = 4/M whole alpha rows per iteration: 4 independent dependency chains; the
+    // admission test is one ballot per key (no min/select sequence)
+    constexpr int R = 4 / M;
+    const double *ap = alpha_tab + (size_t)a * NT;
+    while (r + R * M <= run) {
+        double key[R * M];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            AlphaV av;
+            alpha_vals<FAM>(m, ap + q * NT, av);
+#pragma unroll
+            for (int i = 0; i < M; i++) key[q * M + i] = dmul(combine<FAM>(m, av, sv[i]), m.I);
+        }
+        const double th = tk.adm;
+        unsigned b = 0;
+#pragma unroll
+        for (int i = 0; i < R * M; i++) b |= __ballot_sync(full, key[i] <= th);
+        if (b) {
+#pragma unroll
+            for (int i = 0; i < R * M; i++) tk.offer(true, key[i], idx0 + 32ull * (r + i));
+        }
+        last_a = a + R - 1;
+        last_slot = M - 1;
+        r += R * M;
+        a += R;
+        ap += R * NT;
+    }
+    // remaining whole alpha rows
     while (r + M <= run) {
         AlphaV av;
         alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
         double key[M];
-        bool any = false;
+        unsigned b = 0;
 #pragma unroll
         for (int i = 0; i < M; i++) {
             key[i] = dmul(combine<FAM>(m, av, sv[i]), m.I);
-            any |= key[i] <= tk.thk;
+            b |= __ballot_sync(full, key[i] <= tk.adm);
         }
-        if (__any_sync(full, any)) {
+        if (b) {
 #pragma unroll
             for (int i = 0; i < M; i++) tk.offer(true, key[i], idx0 + 32ull * (r + i));
         }
@@ -824,7 +901,7 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
         AlphaV av;
         alpha_vals<FAM>(m, alpha_tab + (size_t)a * NT, av);
         const double key = dmul(combine<FAM>(m, av, sv[0]), m.I);
-        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, idx0 + 32ull * r);
+        if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, idx0 + 32ull * r);
         last_a = a;
         last_slot = 0;
     }
@@ -888,6 +965,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         Lane L;
         StageT st;
         Mid m;
+        m.reset_memo();
         if ((uint32_t)lane < len) {
             decode(v, u0 + lane, L, cuts, cs);
             if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
@@ -954,6 +1032,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
             run = min(run, nfull - j);
             const bool feas = m.reason == 0;
             if (!DENSE) {
+                tk.refresh();
                 const unsigned fb = __ballot_sync(full, feas);
                 if (fb == 0u) {
                     if (run > 1) {   // no feasible lane: skip the run, closed-form advance
@@ -973,7 +1052,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                         const double key = dmul(inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
                                                                 beta_tab + (size_t)beta_i * NT),
                                                 m.I);
-                        if (__any_sync(full, key <= tk.thk)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
+                        if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
                         beta_i += dB;
                         alpha_i += dA;
                         if (beta_i >= nB) {
@@ -994,7 +1073,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                             key = dmul(inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
                                                        beta_tab + (size_t)beta_i * NT),
                                        m.I);
-                        if (__any_sync(full, feas && key <= tk.thk)) tk.offer(feas, key, g0 + lane + 32ull * (j + r));
+                        if (__any_sync(full, feas && key <= tk.adm)) tk.offer(feas, key, g0 + lane + 32ull * (j + r));
                         if (r + 1 < run) {
                             beta_i += dB;
                             alpha_i += dA;
@@ -1058,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     uint16_t *cuts = &ex->cuts[0][threadIdx.x];
     const unsigned full = 0xffffffffu;
     WarpTopK tk;
-    tk.init(a.k);
+    tk.init(a.k, DENSE ? nullptr : a.gbound);
     unsigned long long cnt = 0;
 
     for (;;) {
@@ -1201,6 +1280,7 @@ __device__ void explain_one(const View &v, const Lane &L, const uint16_t *cuts, 
     constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
     if (PIPE) stage_terms(v, L, cuts, 1, b, st);
     Mid m;
+    m.reset_memo();
     compute_mid<FAM>(v, L, st, m);
     const int NT = v.H->n_tiers;
     const double *arow = at<double>(v.img, v.S->off_alpha) + (size_t)L.d[D_ALPHA] * NT;

@@ -102,6 +102,7 @@ struct LaunchArgs {
     int32_t k, pad;
     paradl_hit *cta_lists;         // [gridDim.x][k] (reduce mode)
     unsigned long long *count;     // feasible count accumulator (reduce mode)
+    unsigned long long *gbound;    // shared top-k admission bound (reduce mode; ~0 = none)
     double *t_iter;                // dense outputs (indexed by global idx - first)
     double *mem;
     uint32_t *bits;

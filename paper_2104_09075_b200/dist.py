@@ -1,0 +1,51 @@
+"""Multi-GPU sweep: tile shards per rank + one all_gather of fixed-size top-k records.
+
+SURVEY §8(e): every rank runs paradl_topk_async on its tile shard (t % world == rank),
+then the (k x 16 B) hit records and the feasible counts are all-gathered (NCCL over
+NVLink on GPUs; gloo on CPU for tests) and every rank merges them with the device merge
+kernel (paradl_merge_topk).  The merge is order-independent, so the result is bit-identical
+to the 1-GPU result.  A hit record is two int64 words: (idx, key bits of the fp64 key).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def gather_topk(hits: torch.Tensor, count: torch.Tensor, group=None):
+    """All-gathers per-rank [k, 2] int64 hit records and [1] int64 counts.
+    Returns (lists [world, k, 2], counts [world])."""
+    ws = dist.get_world_size(group)
+    k = hits.shape[0]
+    lists = torch.empty((ws, k, 2), dtype=torch.int64, device=hits.device)
+    counts = torch.empty(ws, dtype=torch.int64, device=hits.device)
+    if dist.get_backend(group) == "gloo":
+        dist.all_gather(list(lists.unbind(0)), hits.contiguous(), group=group)
+        dist.all_gather(list(counts.view(ws, 1).unbind(0)), count.view(1).contiguous(), group=group)
+    else:
+        dist.all_gather_into_tensor(lists.view(ws, -1), hits.reshape(-1).contiguous(), group=group)
+        dist.all_gather_into_tensor(counts, count.view(1).contiguous(), group=group)
+    return lists, counts
+
+
+def sharded_topk(ctx, spec, first: int, count: int, k: int, out_hits: torch.Tensor, out_count: torch.Tensor,
+                 my_hits: torch.Tensor, my_count: torch.Tensor, group=None, stream=None):
+    """One multi-GPU top-k step on the current device: shard -> all_gather -> device merge.
+    All tensors are int64 on the ctx's device: out_hits/my_hits [k, 2], out_count/my_count [1].
+    Returns (out_hits, out_count, stats) with this rank's H2D bytes and kernel launches."""
+    ws = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ctx.topk_async(spec, first, count, rank, ws, k, my_hits.data_ptr(), my_count.data_ptr(), stream=stream)
+    stats = {"h2d": ctx.stat(0), "launches": ctx.stat(2) + 1}
+    lists, counts = gather_topk(my_hits, my_count, group)
+    ctx.merge_topk(lists.data_ptr(), ws, k, counts.data_ptr(), out_hits.data_ptr(), out_count.data_ptr(),
+                   stream=stream)
+    return out_hits, out_count, stats
+
+
+def decode_hits(hits: torch.Tensor):
+    """[k, 2] int64 records -> list of (idx, key) (host)."""
+    h = hits.detach().cpu()
+    idx = [int(v) & ((1 << 64) - 1) for v in h[:, 0].tolist()]
+    keys = h[:, 1].contiguous().view(torch.float64).tolist()
+    return list(zip(idx, keys))
