@@ -582,18 +582,82 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             memset(&L.back(), 0, sizeof(LaunchArgs));
         }
         LaunchArgs &a = L[li];
-        WorkItem &w = a.work[a.n_work++];
-        w.sub = (int32_t)q;
-        w.family = fam;
-        w.lo = r0 - s0;
-        w.hi = r1 - s0;
-        stride_digits(h, w);
+        // lane-blocked mode for pipeline families with a small alpha/beta block (reduce mode):
+        // the block-aligned middle of the range is mode 1, ragged ends stay mode 0
+        const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD;
+        const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
+        const uint64_t Q = nAB * h.radix[D_LS] * h.radix[D_DIMS] * h.radix[D_S];
+        const uint64_t memo_n = (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]);
+        const uint64_t lo = r0 - s0, hi = r1 - s0;
+        uint64_t b0 = lo, b1 = lo;   // [b0, b1): mode-1 part
+        if (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 31) && a.n_work + 3 <= kMaxSub) {
+            b0 = (lo + Q - 1) / Q * Q;
+            b1 = hi / Q * Q;
+            if (b1 <= b0) b0 = b1 = lo;
+        }
+        const uint64_t parts[3][2] = {{lo, b0}, {b0, b1}, {b1, hi}};
+        for (int pi = 0; pi < 3; pi++) {
+            if (pi == 0 && b1 == b0) {   // whole range in mode 0
+                WorkItem &w = a.work[a.n_work++];
+                w.sub = (int32_t)q;
+                w.family = fam;
+                w.lo = lo;
+                w.hi = hi;
+                stride_digits(h, w);
+                break;
+            }
+            if (parts[pi][0] >= parts[pi][1]) continue;
+            WorkItem &w = a.work[a.n_work++];
+            w.sub = (int32_t)q;
+            w.family = fam;
+            w.lo = parts[pi][0];
+            w.hi = parts[pi][1];
+            if (pi == 1) {
+                w.mode = 1;
+                memset(w.inc, 0, sizeof w.inc);
+                w.inc_part = 1;
+                w.inc_top = D_PART;
+                w.memo_n = (uint32_t)memo_n;
+                w.memo_off = a.memo_bytes;
+                a.memo_bytes += (uint32_t)align16(memo_n * sizeof(double));
+            } else {
+                stride_digits(h, w);
+            }
+        }
         if (fam == PARADL_SPATIAL || fam == PARADL_DS) {
             HaloJob &j = hj.job[hj.n_jobs++];
             j.sub = (int32_t)q;
             j.n_entries = (int32_t)(h.radix[D_DIMS] * h.radix[D_LS]);
             j.entry_base = (int32_t)halo_entries;
             halo_entries += j.n_entries;
+        }
+    }
+    // lane-blocked work items go to their own launches (kernel template BLK = true)
+    std::vector<int> blk_of(L.size(), 0);
+    {
+        const size_t n0 = L.size();
+        for (size_t li = 0; li < n0; li++) {
+            LaunchArgs blk{};
+            memset(&blk, 0, sizeof blk);
+            LaunchArgs keep{};
+            memset(&keep, 0, sizeof keep);
+            for (int i = 0; i < L[li].n_work; i++) {
+                const WorkItem &w = L[li].work[i];
+                if (w.mode == 1) blk.work[blk.n_work++] = w;
+                else keep.work[keep.n_work++] = w;
+            }
+            if (blk.n_work == 0) continue;
+            blk.memo_bytes = L[li].memo_bytes;
+            keep.memo_bytes = 0;
+            if (keep.n_work == 0) {
+                L[li] = blk;
+                blk_of[li] = 1;
+            } else {
+                L[li] = keep;
+                L.push_back(blk);
+                fam_of.push_back(fam_of[li]);
+                blk_of.push_back(1);
+            }
         }
     }
     const size_t nl = L.size();
@@ -610,22 +674,36 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     }
     // tiles and grids
     std::vector<int> grids(nl);
+    std::vector<size_t> smems(nl);
     size_t total_ctas = 0;
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
-        const int nb = max_blocks_per_sm(fam_of[li], dense, smem);
-        if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smem);
+        smems[li] = smem + a.memo_bytes;
+        const int nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li] != 0, smems[li]);
+        if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smems[li]);
         const int grid_max = c->n_sm * nb;
         const uint64_t warps = (uint64_t)grid_max * kWarps;
         uint64_t tiles = 0;
         for (int i = 0; i < a.n_work; i++) {
             WorkItem &w = a.work[i];
             const uint64_t range = w.hi - w.lo;
-            // >= ~8 tiles per warp for balance, 32..32768 configurations per tile
-            uint64_t steps = range / (32ull * warps * 8ull);
-            steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
-            w.steps = (uint32_t)steps;
-            w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
+            if (w.mode == 1) {
+                const SubHdr &h = P.subs[w.sub].hdr;
+                const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
+                                   h.radix[D_S];
+                const uint64_t nblk = range / Q;
+                // >= ~8 tiles per warp; 1..256 partitions per lane per tile
+                uint64_t cper = nblk / (32ull * warps * 8ull);
+                cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
+                w.steps = (uint32_t)cper;
+                w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
+            } else {
+                // >= ~8 tiles per warp for balance, 32..32768 configurations per tile
+                uint64_t steps = range / (32ull * warps * 8ull);
+                steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
+                w.steps = (uint32_t)steps;
+                w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
+            }
             w.tile_base = tiles;
             tiles += w.n_tiles;
         }
@@ -682,7 +760,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             ls = c->streams[li];
             CUDA_TRY(c, cudaStreamWaitEvent(ls, c->fork_ev, 0));
         }
-        CUDA_TRY(c, launch_sweep(fam_of[li], dense, a, grids[li], smem, ls));
+        CUDA_TRY(c, launch_sweep(fam_of[li], dense, blk_of[li] != 0, a, grids[li], smems[li], ls));
         c->stat_launches++;
         if (fork) CUDA_TRY(c, cudaEventRecord(c->events[li], ls));
         cta_off += grids[li];

@@ -1125,7 +1125,163 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
     
 }
 
-template <int FAM, bool DENSE>
+// ------------------------------------------------------------------ lane-blocked tiles (pipeline families)
+// For sub-sweeps whose alpha/beta block is small (e.g. cfg5: 2x2) a lane owns whole
+// partitions: lane l of tile t evaluates partitions [t*32c + l*c, +c) of the work item's
+// block-aligned range, each with its inner S x dims x Ls x alpha x beta block.  Terms are
+// hoisted per partition (stage sums), per dims value (p, tiers, GE) and per S (comp, P2P);
+// the fp64 trees are those of compute_mid / inner_fast, so results are bit-identical.
+// memo = this work item's smem table [n_b][n_S + n_dims]: b/S and D/(b*dims0).
+template <int FAM>
+__device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                                  uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo) {
+    const View v = make_view(smem, w.sub);
+    const SubHdr *S = v.S;
+    const ImgHdr *H = v.H;
+    const ModelHdr *M = v.M;
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int NT = H->n_tiers;
+    const uint32_t nB = S->radix[D_BETA], nA = S->radix[D_ALPHA], nL = S->radix[D_LS];
+    const uint32_t nD = S->radix[D_DIMS], nS = S->radix[D_S];
+    const uint32_t nLAB = nL * nA * nB;
+    const uint64_t Q = (uint64_t)nS * nD * nLAB;
+    const uint64_t nblk = (w.hi - w.lo) / Q;
+    const uint64_t c = w.steps;
+    const uint64_t blk0 = (tile * 32 + lane) * c;
+    const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
+    const uint32_t iters = __reduce_max_sync(full, (uint32_t)nmine);
+    const double *alpha_tab = at<double>(v.img, S->off_alpha);
+    const double *beta_tab = at<double>(v.img, S->off_beta);
+    const int32_t *Sv = at<int32_t>(v.img, S->off_S);
+    const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
+    const int64_t delta = H->delta;
+    Lane L;
+    StageT st;
+    if (nmine) decode(v, w.lo + blk0 * Q, L, cuts, kThreads);
+    double R_memo = -1.0, tau = 0.0;
+    for (uint32_t it = 0; it < iters; it++) {
+        const bool act = it < nmine;
+        int64_t b = 1, ns = 1;
+        double cap = 0.0, FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, comp_lp = 0.0, lp_na = 0.0, lp_s = 0.0;
+        uint32_t rp = PARADL_R_SCALING;   // partition-level reason (inactive lanes: infeasible)
+        int ts = 0;
+        const double *mrow = memo;
+        if (act) {
+            b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
+            cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
+            const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
+            if (R != R_memo) {
+                R_memo = R;
+                tau = ddiv(1.0, R);
+            }
+            stage_terms(v, L, cuts, kThreads, b, st);
+            ns = L.ns;
+            rp = 0;
+            ts = tier_of(H, ns);
+            rp |= flag_tier(ts);
+            ts = max(ts, 0);
+            const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
+            if (!(memv <= cap)) rp |= PARADL_R_MEMORY;
+            if (FAM == PARADL_LAYERPURE) {
+                comp_lp = comp_term(b * M->FB, M->WU, 1, 1, tau);
+                lp_na = ns > 1 ? i2d(ns - 1) : 0.0;
+                lp_s = ns > 1 ? i2d(delta * b * st.sumY) : 0.0;
+            } else {
+                FBs = i2d(st.maxF + st.maxB);
+                Utau = dmul(i2d(st.maxU), tau);
+                dmaxY = i2d(delta * st.maxY);
+                if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
+            }
+            mrow = memo + (size_t)L.d[D_B] * (nS + nD);
+        }
+        const uint64_t gblk = S->offset + w.lo + (blk0 + it) * Q;   // global index of the block's first config
+        for (uint32_t iD = 0; iD < nD; iD++) {
+            // per dims value: p = s*p_d, tiers, GE
+            const int64_t pd = FAM == PARADL_PD ? dmv[4 * iD] : 1;
+            const double I = mrow[nS + iD];
+            uint32_t rd = rp;
+            double ge_c = 0.0, ge_s = 0.0;
+            int ge_t = 0;
+            if (FAM == PARADL_PD && act) {
+                const int tp = tier_of(H, ns * pd);
+                rd |= flag_tier(tp);
+                const ARt g = make_ar(H, pd, mW, ddiv(mW, i2d(pd)), tp);
+                if (g.on) {
+                    ge_c = g.c;
+                    ge_s = g.s;
+                }
+                ge_t = max(tp, 0);
+            }
+            for (uint32_t iS = 0; iS < nS; iS++) {
+                const int64_t Sg = Sv[iS];
+                uint32_t r = rd;
+                if (Sg < 1 || Sg > b) r |= PARADL_R_SEGMENTS;
+                double comp = comp_lp, pp_c = 0.0, pp_s = 0.0;
+                if (FAM != PARADL_LAYERPURE && act) {
+                    const double bS = mrow[iS];
+                    const double cseg = dmul(i2d(ns + Sg - 1), bS);
+                    comp = dadd(dmul(dmul(cseg, FBs), tau), Utau);
+                    if (ns > 1) {
+                        pp_c = i2d(2 * (ns + Sg - 2));
+                        pp_s = dmul(bS, dmaxY);
+                    }
+                }
+                const bool feas = act && r == 0;
+                cnt += feas ? nLAB : 0u;
+                if (__ballot_sync(full, feas) == 0u) continue;
+                const uint64_t base = gblk + (uint64_t)(iS * nD + iD) * nLAB;
+                for (uint32_t iL = 0; iL < nL; iL++)
+                    for (uint32_t ia = 0; ia < nA; ia++) {
+                        const double *arow = alpha_tab + (size_t)ia * NT;
+                        const double aval_pp = FAM == PARADL_LAYERPURE ? dmul(lp_na, arow[ts]) : arow[ts];
+                        for (uint32_t ib = 0; ib < nB; ib++) {
+                            const double *brow = beta_tab + (size_t)ib * NT;
+                            double t = comp;
+                            if (FAM == PARADL_PD) t = dadd(t, dmul(ge_c, dadd(arow[ge_t], dmul(ge_s, brow[ge_t]))));
+                            if (FAM == PARADL_LAYERPURE)
+                                t = dadd(t, dmul(2.0, dadd(aval_pp, dmul(lp_s, brow[ts]))));
+                            else
+                                t = dadd(t, dmul(pp_c, dadd(aval_pp, dmul(pp_s, brow[ts]))));
+                            const double key = feas ? dmul(t, I) : CUDART_INF;
+                            if (__any_sync(full, key <= tk.adm))
+                                tk.offer(feas, key, base + (uint64_t)(iL * nA + ia) * nB + ib);
+                        }
+                    }
+            }
+        }
+        tk.refresh();
+        if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next partition (inc_part = 1)
+    }
+}
+
+// Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
+// with the same fp64 operations compute_mid uses.
+__device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base) {
+    for (int wi = 0; wi < a.n_work; wi++) {
+        const WorkItem &w = a.work[wi];
+        if (w.mode != 1) continue;
+        const View v = make_view(smem, w.sub);
+        const SubHdr *S = v.S;
+        const uint32_t nS = S->radix[D_S], nD = S->radix[D_DIMS];
+        double *tab = memo_base + w.memo_off / sizeof(double);
+        const int64_t *bv = at<int64_t>(v.img, S->off_b);
+        const int32_t *Sv = at<int32_t>(v.img, S->off_S);
+        const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
+        for (uint32_t e = threadIdx.x; e < w.memo_n; e += blockDim.x) {
+            const uint32_t ib = e / (nS + nD), j = e - ib * (nS + nD);
+            const int64_t b = bv[ib];
+            if (j < nS) tab[e] = ddiv(i2d(b), i2d(Sv[j]));
+            else {
+                const int64_t pd = w.family == PARADL_PD ? dmv[4 * (j - nS)] : 1;
+                tab[e] = ddiv(i2d(v.M->D), i2d(b * pd));
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int FAM, bool DENSE, bool BLK>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t mbar;
@@ -1139,6 +1295,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     WarpTopK tk;
     tk.init(a.k, DENSE ? nullptr : a.gbound);
     unsigned long long cnt = 0;
+    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
+    double *memo = reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra));
+    if (BLK) build_memo(a, smem, memo);
 
     for (;;) {
         unsigned long long t = 0;
@@ -1149,7 +1308,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         int wi = 0;
         while (wi + 1 < a.n_work && T >= a.work[wi + 1].tile_base) wi++;
         const WorkItem &w = a.work[wi];
-        tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
+        if (BLK)
+            tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo);
+        else
+            tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
     }
 
     if (!DENSE) {
@@ -1530,9 +1692,18 @@ cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t 
 // ------------------------------------------------------------------ launchers
 size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
-static void *sweep_fn(int family, bool dense) {
+static void *sweep_fn(int family, bool dense, bool blk) {
+    if (blk) {
+        if (dense) return nullptr;
+        switch (family) {
+        case PARADL_PIPELINE: return (void *)sweep_kernel<PARADL_PIPELINE, false, true>;
+        case PARADL_LAYERPURE: return (void *)sweep_kernel<PARADL_LAYERPURE, false, true>;
+        case PARADL_PD: return (void *)sweep_kernel<PARADL_PD, false, true>;
+        default: return nullptr;
+        }
+    }
 #define PARADL_CASE(F) \
-    case F: return dense ? (void *)sweep_kernel<F, true> : (void *)sweep_kernel<F, false>;
+    case F: return dense ? (void *)sweep_kernel<F, true, false> : (void *)sweep_kernel<F, false, false>;
     switch (family) {
         PARADL_CASE(PARADL_SERIAL)
         PARADL_CASE(PARADL_DATA)
@@ -1549,8 +1720,8 @@ static void *sweep_fn(int family, bool dense) {
 #undef PARADL_CASE
 }
 
-int max_blocks_per_sm(int family, bool dense, size_t smem) {
-    void *fn = sweep_fn(family, dense);
+int max_blocks_per_sm(int family, bool dense, bool blk, size_t smem) {
+    void *fn = sweep_fn(family, dense, blk);
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     int nb = 0;
@@ -1558,8 +1729,9 @@ int max_blocks_per_sm(int family, bool dense, size_t smem) {
     return nb;
 }
 
-cudaError_t launch_sweep(int family, bool dense, const LaunchArgs &a, int grid, size_t smem, cudaStream_t st) {
-    void *fn = sweep_fn(family, dense);
+cudaError_t launch_sweep(int family, bool dense, bool blk, const LaunchArgs &a, int grid, size_t smem,
+                         cudaStream_t st) {
+    void *fn = sweep_fn(family, dense, blk);
     if (!fn) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

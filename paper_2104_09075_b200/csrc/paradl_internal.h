@@ -81,13 +81,15 @@ static_assert(sizeof(HaloEntry) == 32, "HaloEntry layout");
 // the launch's global tile space (all work items concatenated, spec order).
 struct WorkItem {
     int32_t sub, family;
-    uint32_t steps;
+    uint32_t steps;                // mode 0: steps of 32 configs per tile; mode 1: partitions per lane per tile
     int32_t inc_top;               // highest digit with a non-zero stride increment
     uint64_t lo, hi, n_tiles, tile_base;
-    uint32_t inc[kDigits];         // mixed-radix digits of the lane stride 32
-    uint32_t pad;
+    uint32_t inc[kDigits];         // mixed-radix digits of the lane stride (32 configs, or 1 partition)
+    int32_t mode;                  // 0: lane-strided (lanes = 32 consecutive configs); 1: lane-blocked
+                                   // (pipeline families: each lane owns whole partitions, [lo,hi) aligned)
     uint64_t inc_part;
     const HaloEntry *halo;         // spatial / ds: [n_dims][n_Ls] table (device global), else null
+    uint32_t memo_off, memo_n;     // mode 1: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
@@ -95,6 +97,8 @@ struct LaunchArgs {
     const uint8_t *img;            // device image
     uint32_t img_bytes;            // multiple of 16
     int32_t n_work;
+    uint32_t memo_bytes;           // lane-blocked memo tables after SmemExtra (multiple of 16)
+    uint32_t pad_;
     uint64_t first;                // global index of dense element 0
     uint64_t total_tiles;
     int32_t shard, n_shards;
@@ -124,8 +128,9 @@ struct HaloJobs {
 // launchers implemented in kernels.cu
 cudaError_t launch_prep_model(const paradl_layer *d_rows, int32_t G, int64_t D, uint8_t *d_block,
                               const ModelHdr &layout, cudaStream_t st);
-cudaError_t launch_sweep(int family, bool dense, const LaunchArgs &a, int grid, size_t smem, cudaStream_t st);
-int max_blocks_per_sm(int family, bool dense, size_t smem);
+cudaError_t launch_sweep(int family, bool dense, bool blk, const LaunchArgs &a, int grid, size_t smem,
+                         cudaStream_t st);
+int max_blocks_per_sm(int family, bool dense, bool blk, size_t smem);
 size_t sweep_smem_extra();
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
