@@ -582,17 +582,23 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             memset(&L.back(), 0, sizeof(LaunchArgs));
         }
         LaunchArgs &a = L[li];
-        // lane-blocked mode for pipeline families with a small alpha/beta block (reduce mode):
-        // the block-aligned middle of the range is mode 1, ragged ends stay mode 0
+        // lane-blocked modes for pipeline families with a small alpha/beta block (reduce mode):
+        // the block-aligned middle of the range is mode 1 (COMB, or MASK with G < 10) or mode 2
+        // (MASK, 256-mask blocks with the low-bit table); ragged ends stay mode 0
         const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD;
         const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
         const uint64_t Q = nAB * h.radix[D_LS] * h.radix[D_DIMS] * h.radix[D_S];
         const uint64_t memo_n = (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]);
+        const bool mask2 = h.part_mode == PARADL_PART_MASK && h.G >= 10 && h.radix[D_B] <= 2;
+        const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22) && a.n_work + 3 <= kMaxSub)
+                             ? (mask2 ? 2 : 1)
+                             : 0;
+        const uint64_t unit = mode == 2 ? Q << 8 : Q;
         const uint64_t lo = r0 - s0, hi = r1 - s0;
-        uint64_t b0 = lo, b1 = lo;   // [b0, b1): mode-1 part
-        if (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 31) && a.n_work + 3 <= kMaxSub) {
-            b0 = (lo + Q - 1) / Q * Q;
-            b1 = hi / Q * Q;
+        uint64_t b0 = lo, b1 = lo;   // [b0, b1): blocked part
+        if (mode) {
+            b0 = (lo + unit - 1) / unit * unit;
+            b1 = hi / unit * unit;
             if (b1 <= b0) b0 = b1 = lo;
         }
         const uint64_t parts[3][2] = {{lo, b0}, {b0, b1}, {b1, hi}};
@@ -613,13 +619,17 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             w.lo = parts[pi][0];
             w.hi = parts[pi][1];
             if (pi == 1) {
-                w.mode = 1;
+                w.mode = mode;
                 memset(w.inc, 0, sizeof w.inc);
-                w.inc_part = 1;
+                w.inc_part = mode == 2 ? 256 : 1;
                 w.inc_top = D_PART;
                 w.memo_n = (uint32_t)memo_n;
                 w.memo_off = a.memo_bytes;
                 a.memo_bytes += (uint32_t)align16(memo_n * sizeof(double));
+                if (mode == 2) {
+                    w.low_off = a.low_bytes / 64;
+                    a.low_bytes += h.radix[D_B] * 256u * 64u;
+                }
             } else {
                 stride_digits(h, w);
             }
@@ -632,31 +642,35 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             halo_entries += j.n_entries;
         }
     }
-    // lane-blocked work items go to their own launches (kernel template BLK = true)
+    // lane-blocked work items go to their own launches (kernel template BLK = 1 or 2)
     std::vector<int> blk_of(L.size(), 0);
     {
         const size_t n0 = L.size();
         for (size_t li = 0; li < n0; li++) {
-            LaunchArgs blk{};
-            memset(&blk, 0, sizeof blk);
-            LaunchArgs keep{};
-            memset(&keep, 0, sizeof keep);
+            LaunchArgs by_mode[3];
+            for (auto &x : by_mode) memset(&x, 0, sizeof x);
             for (int i = 0; i < L[li].n_work; i++) {
                 const WorkItem &w = L[li].work[i];
-                if (w.mode == 1) blk.work[blk.n_work++] = w;
-                else keep.work[keep.n_work++] = w;
+                by_mode[w.mode].work[by_mode[w.mode].n_work++] = w;
             }
-            if (blk.n_work == 0) continue;
-            blk.memo_bytes = L[li].memo_bytes;
-            keep.memo_bytes = 0;
-            if (keep.n_work == 0) {
-                L[li] = blk;
-                blk_of[li] = 1;
-            } else {
-                L[li] = keep;
-                L.push_back(blk);
-                fam_of.push_back(fam_of[li]);
-                blk_of.push_back(1);
+            bool first = true;
+            const uint32_t memo_bytes = L[li].memo_bytes, low_bytes = L[li].low_bytes;
+            for (int md = 0; md < 3; md++) {
+                LaunchArgs &x = by_mode[md];
+                if (x.n_work == 0) continue;
+                if (md) {
+                    x.memo_bytes = memo_bytes;
+                    x.low_bytes = low_bytes;
+                }
+                if (first) {
+                    L[li] = x;
+                    blk_of[li] = md;
+                    first = false;
+                } else {
+                    L.push_back(x);
+                    fam_of.push_back(fam_of[li]);
+                    blk_of.push_back(md);
+                }
             }
         }
     }
@@ -678,8 +692,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     size_t total_ctas = 0;
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
-        smems[li] = smem + a.memo_bytes;
-        const int nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li] != 0, smems[li]);
+        smems[li] = smem + a.memo_bytes + a.low_bytes;
+        const int nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li], smems[li]);
         if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smems[li]);
         const int grid_max = c->n_sm * nb;
         const uint64_t warps = (uint64_t)grid_max * kWarps;
@@ -687,11 +701,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         for (int i = 0; i < a.n_work; i++) {
             WorkItem &w = a.work[i];
             const uint64_t range = w.hi - w.lo;
-            if (w.mode == 1) {
+            if (w.mode != 0) {
                 const SubHdr &h = P.subs[w.sub].hdr;
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
-                const uint64_t nblk = range / Q;
+                const uint64_t nblk = range / (w.mode == 2 ? Q << 8 : Q);
                 // >= ~8 tiles per warp; 1..256 partitions per lane per tile
                 uint64_t cper = nblk / (32ull * warps * 8ull);
                 cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
@@ -760,7 +774,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             ls = c->streams[li];
             CUDA_TRY(c, cudaStreamWaitEvent(ls, c->fork_ev, 0));
         }
-        CUDA_TRY(c, launch_sweep(fam_of[li], dense, blk_of[li] != 0, a, grids[li], smems[li], ls));
+        CUDA_TRY(c, launch_sweep(fam_of[li], dense, blk_of[li], a, grids[li], smems[li], ls));
         c->stat_launches++;
         if (fork) CUDA_TRY(c, cudaEventRecord(c->events[li], ls));
         cta_off += grids[li];

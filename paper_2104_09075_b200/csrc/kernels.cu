@@ -1127,140 +1127,279 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
 
 // ------------------------------------------------------------------ lane-blocked tiles (pipeline families)
 // For sub-sweeps whose alpha/beta block is small (e.g. cfg5: 2x2) a lane owns whole
-// partitions: lane l of tile t evaluates partitions [t*32c + l*c, +c) of the work item's
-// block-aligned range, each with its inner S x dims x Ls x alpha x beta block.  Terms are
-// hoisted per partition (stage sums), per dims value (p, tiers, GE) and per S (comp, P2P);
-// the fp64 trees are those of compute_mid / inner_fast, so results are bit-identical.
-// memo = this work item's smem table [n_b][n_S + n_dims]: b/S and D/(b*dims0).
+// partitions, each with its inner S x dims x Ls x alpha x beta block.  Terms are hoisted
+// per partition (stage sums), per dims value (p, tiers, GE) and per S (comp, P2P); the
+// fp64 trees are those of compute_mid / inner_fast, so results are bit-identical.
+// memo = the work item's smem table [n_b][n_S + n_dims]: b/S and D/(b*dims0).
+struct BlkCtx {
+    View v;
+    const double *alpha_tab, *beta_tab, *memo;
+    const int32_t *Sv, *dmv;
+    uint32_t nB, nA, nL, nD, nS, nLAB;
+    uint64_t Q;
+    double R_memo, tau;
+};
+
+__device__ __forceinline__ BlkCtx make_blk(const WorkItem &w, uint8_t *smem, const double *memo) {
+    BlkCtx C;
+    C.v = make_view(smem, w.sub);
+    const SubHdr *S = C.v.S;
+    C.alpha_tab = at<double>(C.v.img, S->off_alpha);
+    C.beta_tab = at<double>(C.v.img, S->off_beta);
+    C.Sv = at<int32_t>(C.v.img, S->off_S);
+    C.dmv = at<int32_t>(C.v.img, S->off_dims);
+    C.memo = memo + w.memo_off / sizeof(double);
+    C.nB = S->radix[D_BETA];
+    C.nA = S->radix[D_ALPHA];
+    C.nL = S->radix[D_LS];
+    C.nD = S->radix[D_DIMS];
+    C.nS = S->radix[D_S];
+    C.nLAB = C.nL * C.nA * C.nB;
+    C.Q = (uint64_t)C.nS * C.nD * C.nLAB;
+    C.R_memo = -1.0;
+    C.tau = 0.0;
+    return C;
+}
+
+// Evaluates one partition (stage terms st, ns stages) and its inner block for the lane;
+// gblk = global index of the block's first configuration.  Whole warp (act per lane).
 template <int FAM>
-__device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
-                                  uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo) {
-    const View v = make_view(smem, w.sub);
+__device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &L, const StageT &st, int64_t ns,
+                                               uint64_t gblk, WarpTopK &tk, unsigned long long &cnt) {
+    const View &v = C.v;
     const SubHdr *S = v.S;
     const ImgHdr *H = v.H;
     const ModelHdr *M = v.M;
-    const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int NT = H->n_tiers;
-    const uint32_t nB = S->radix[D_BETA], nA = S->radix[D_ALPHA], nL = S->radix[D_LS];
-    const uint32_t nD = S->radix[D_DIMS], nS = S->radix[D_S];
-    const uint32_t nLAB = nL * nA * nB;
-    const uint64_t Q = (uint64_t)nS * nD * nLAB;
-    const uint64_t nblk = (w.hi - w.lo) / Q;
+    const int64_t delta = H->delta;
+    int64_t b = 1;
+    double FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, comp_lp = 0.0, lp_na = 0.0, lp_s = 0.0;
+    uint32_t rp = PARADL_R_SCALING;   // partition-level reason (inactive lanes: infeasible)
+    int ts = 0;
+    const double *mrow = C.memo;
+    if (act) {
+        b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
+        const double cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
+        const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
+        if (R != C.R_memo) {
+            C.R_memo = R;
+            C.tau = ddiv(1.0, R);
+        }
+        rp = 0;
+        ts = tier_of(H, ns);
+        rp |= flag_tier(ts);
+        ts = max(ts, 0);
+        const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
+        if (!(memv <= cap)) rp |= PARADL_R_MEMORY;
+        if (FAM == PARADL_LAYERPURE) {
+            comp_lp = comp_term(b * M->FB, M->WU, 1, 1, C.tau);
+            lp_na = ns > 1 ? i2d(ns - 1) : 0.0;
+            lp_s = ns > 1 ? i2d(delta * b * st.sumY) : 0.0;
+        } else {
+            FBs = i2d(st.maxF + st.maxB);
+            Utau = dmul(i2d(st.maxU), C.tau);
+            dmaxY = i2d(delta * st.maxY);
+            if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
+        }
+        mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
+    }
+    const double tau = C.tau;
+    for (uint32_t iD = 0; iD < C.nD; iD++) {
+        // per dims value: p = s*p_d, tiers, GE
+        const int64_t pd = FAM == PARADL_PD ? C.dmv[4 * iD] : 1;
+        const double I = mrow[C.nS + iD];
+        uint32_t rd = rp;
+        double ge_c = 0.0, ge_s = 0.0;
+        int ge_t = 0;
+        if (FAM == PARADL_PD && act) {
+            const int tp = tier_of(H, ns * pd);
+            rd |= flag_tier(tp);
+            const ARt g = make_ar(H, pd, mW, ddiv(mW, i2d(pd)), tp);
+            if (g.on) {
+                ge_c = g.c;
+                ge_s = g.s;
+            }
+            ge_t = max(tp, 0);
+        }
+        for (uint32_t iS = 0; iS < C.nS; iS++) {
+            const int64_t Sg = C.Sv[iS];
+            uint32_t r = rd;
+            if (Sg < 1 || Sg > b) r |= PARADL_R_SEGMENTS;
+            double comp = comp_lp, pp_c = 0.0, pp_s = 0.0;
+            if (FAM != PARADL_LAYERPURE && act) {
+                const double bS = mrow[iS];
+                const double cseg = dmul(i2d(ns + Sg - 1), bS);
+                comp = dadd(dmul(dmul(cseg, FBs), tau), Utau);
+                if (ns > 1) {
+                    pp_c = i2d(2 * (ns + Sg - 2));
+                    pp_s = dmul(bS, dmaxY);
+                }
+            }
+            const bool feas = act && r == 0;
+            cnt += feas ? C.nLAB : 0u;
+            if (__ballot_sync(full, feas) == 0u) continue;
+            const uint64_t base = gblk + (uint64_t)(iS * C.nD + iD) * C.nLAB;
+            for (uint32_t iL = 0; iL < C.nL; iL++)
+                for (uint32_t ia = 0; ia < C.nA; ia++) {
+                    const double *arow = C.alpha_tab + (size_t)ia * NT;
+                    const double aval_pp = FAM == PARADL_LAYERPURE ? dmul(lp_na, arow[ts]) : arow[ts];
+                    for (uint32_t ib = 0; ib < C.nB; ib++) {
+                        const double *brow = C.beta_tab + (size_t)ib * NT;
+                        double t = comp;
+                        if (FAM == PARADL_PD) t = dadd(t, dmul(ge_c, dadd(arow[ge_t], dmul(ge_s, brow[ge_t]))));
+                        if (FAM == PARADL_LAYERPURE)
+                            t = dadd(t, dmul(2.0, dadd(aval_pp, dmul(lp_s, brow[ts]))));
+                        else
+                            t = dadd(t, dmul(pp_c, dadd(aval_pp, dmul(pp_s, brow[ts]))));
+                        const double key = feas ? dmul(t, I) : CUDART_INF;
+                        if (__any_sync(full, key <= tk.adm))
+                            tk.offer(feas, key, base + (uint64_t)(iL * C.nA + ia) * C.nB + ib);
+                    }
+                }
+        }
+    }
+}
+
+// Mode 1: lane l of tile t owns partitions [t*32c + l*c, +c) of the block-aligned range;
+// stage terms by prefix differences, successor between partitions.
+template <int FAM>
+__device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                                  uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo) {
+    BlkCtx C = make_blk(w, smem, memo);
+    const int lane = threadIdx.x & 31;
+    const uint64_t nblk = (w.hi - w.lo) / C.Q;
     const uint64_t c = w.steps;
     const uint64_t blk0 = (tile * 32 + lane) * c;
     const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
-    const uint32_t iters = __reduce_max_sync(full, (uint32_t)nmine);
-    const double *alpha_tab = at<double>(v.img, S->off_alpha);
-    const double *beta_tab = at<double>(v.img, S->off_beta);
-    const int32_t *Sv = at<int32_t>(v.img, S->off_S);
-    const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
-    const int64_t delta = H->delta;
+    const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
     Lane L;
     StageT st;
-    if (nmine) decode(v, w.lo + blk0 * Q, L, cuts, kThreads);
-    double R_memo = -1.0, tau = 0.0;
+    if (nmine) decode(C.v, w.lo + blk0 * C.Q, L, cuts, kThreads);
     for (uint32_t it = 0; it < iters; it++) {
         const bool act = it < nmine;
-        int64_t b = 1, ns = 1;
-        double cap = 0.0, FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, comp_lp = 0.0, lp_na = 0.0, lp_s = 0.0;
-        uint32_t rp = PARADL_R_SCALING;   // partition-level reason (inactive lanes: infeasible)
-        int ts = 0;
-        const double *mrow = memo;
+        int64_t ns = 1;
         if (act) {
-            b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
-            cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
-            const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
-            if (R != R_memo) {
-                R_memo = R;
-                tau = ddiv(1.0, R);
-            }
-            stage_terms(v, L, cuts, kThreads, b, st);
+            stage_terms(C.v, L, cuts, kThreads, at<int64_t>(C.v.img, C.v.S->off_b)[L.d[D_B]], st);
             ns = L.ns;
-            rp = 0;
-            ts = tier_of(H, ns);
-            rp |= flag_tier(ts);
-            ts = max(ts, 0);
-            const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
-            if (!(memv <= cap)) rp |= PARADL_R_MEMORY;
-            if (FAM == PARADL_LAYERPURE) {
-                comp_lp = comp_term(b * M->FB, M->WU, 1, 1, tau);
-                lp_na = ns > 1 ? i2d(ns - 1) : 0.0;
-                lp_s = ns > 1 ? i2d(delta * b * st.sumY) : 0.0;
-            } else {
-                FBs = i2d(st.maxF + st.maxB);
-                Utau = dmul(i2d(st.maxU), tau);
-                dmaxY = i2d(delta * st.maxY);
-                if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
-            }
-            mrow = memo + (size_t)L.d[D_B] * (nS + nD);
         }
-        const uint64_t gblk = S->offset + w.lo + (blk0 + it) * Q;   // global index of the block's first config
-        for (uint32_t iD = 0; iD < nD; iD++) {
-            // per dims value: p = s*p_d, tiers, GE
-            const int64_t pd = FAM == PARADL_PD ? dmv[4 * iD] : 1;
-            const double I = mrow[nS + iD];
-            uint32_t rd = rp;
-            double ge_c = 0.0, ge_s = 0.0;
-            int ge_t = 0;
-            if (FAM == PARADL_PD && act) {
-                const int tp = tier_of(H, ns * pd);
-                rd |= flag_tier(tp);
-                const ARt g = make_ar(H, pd, mW, ddiv(mW, i2d(pd)), tp);
-                if (g.on) {
-                    ge_c = g.c;
-                    ge_s = g.s;
-                }
-                ge_t = max(tp, 0);
-            }
-            for (uint32_t iS = 0; iS < nS; iS++) {
-                const int64_t Sg = Sv[iS];
-                uint32_t r = rd;
-                if (Sg < 1 || Sg > b) r |= PARADL_R_SEGMENTS;
-                double comp = comp_lp, pp_c = 0.0, pp_s = 0.0;
-                if (FAM != PARADL_LAYERPURE && act) {
-                    const double bS = mrow[iS];
-                    const double cseg = dmul(i2d(ns + Sg - 1), bS);
-                    comp = dadd(dmul(dmul(cseg, FBs), tau), Utau);
-                    if (ns > 1) {
-                        pp_c = i2d(2 * (ns + Sg - 2));
-                        pp_s = dmul(bS, dmaxY);
+        eval_partition<FAM>(C, act, L, st, ns, C.v.S->offset + w.lo + (blk0 + it) * C.Q, tk, cnt);
+        tk.refresh();
+        if (it + 1 < nmine) advance(w, C.v, L, cuts, kThreads);   // next partition (inc_part = 1)
+    }
+}
+
+// ------------------------------------------------------------------ mask mode with a low-bit table
+// Mode 2 (MASK partitions, G >= 10): lane owns aligned blocks of 256 consecutive masks, so
+// bits 8.. are fixed within a block.  Stages whose rows all lie among the first 9 rows
+// depend only on the low 8 bits: their maxima come from a per-CTA table over the 256
+// patterns.  Stages after the first high cut are evaluated once per block; per mask only
+// the stage straddling bit 8 (from the last low cut to the first high cut) is formed.
+// All quantities are exact int64 sums / maxima, so the composition equals stage_terms.
+constexpr int kLowBits = 8;
+struct LowE {
+    int64_t F, B, U, W, memI, maxY, sumY;
+    int32_t e_last, pop;
+};
+static_assert(sizeof(LowE) == 64, "LowE layout");
+
+template <int FAM>
+__device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                               uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
+                               const LowE *lowtab) {
+    BlkCtx C = make_blk(w, smem, memo);
+    const View &v = C.v;
+    const ModelHdr *M = v.M;
+    const int lane = threadIdx.x & 31;
+    const int G = M->G;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+    const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+    const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    const uint64_t span = C.Q << kLowBits;                 // configs per 256-mask block
+    const uint64_t nblk = (w.hi - w.lo) / span;
+    const uint64_t c = w.steps;
+    const uint64_t blk0 = (tile * 32 + lane) * c;
+    const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
+    const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
+    Lane L;
+    if (nmine) decode(v, w.lo + blk0 * span, L, cuts, kThreads);
+    for (uint32_t it = 0; it < iters; it++) {
+        const bool act = it < nmine;
+        // high part of this block: stages after the first high cut
+        const uint64_t hi_mask = L.part & ~(((uint64_t)1 << kLowBits) - 1);
+        int64_t hF = 0, hB = 0, hU = 0, hW = 0, hM = 0, hY = 0, hS = 0;
+        int c_h = G;
+        int hpop = 0;
+        int64_t b = 1;
+        const LowE *lt = lowtab;
+        if (act) {
+            b = at<int64_t>(v.img, v.S->off_b)[L.d[D_B]];
+            lt = lowtab + (size_t)L.d[D_B] * (1 << kLowBits);
+            uint64_t m = hi_mask;
+            hpop = __popcll(m);
+            if (m) {
+                c_h = __ffsll((long long)m);
+                m &= m - 1;
+                int beg = c_h;
+                hY = Y[c_h - 1];
+                hS = Y[c_h - 1];
+                for (;;) {
+                    int end;
+                    if (m) {
+                        end = __ffsll((long long)m);
+                        m &= m - 1;
+                    } else {
+                        end = G;
                     }
+                    const int64_t F = PF[end] - PF[beg], Bw = PB[end] - PB[beg], U = PU[end] - PU[beg];
+                    const int64_t Wt = PW[end] - PW[beg], XY = PX[end] - PX[beg], BI = PI[end] - PI[beg];
+                    hF = max(hF, F);
+                    hB = max(hB, Bw);
+                    hU = max(hU, U);
+                    hW = max(hW, Wt);
+                    hM = max(hM, 2 * b * XY + 2 * Wt + BI);
+                    if (end == G) break;
+                    hY = max(hY, Y[end - 1]);
+                    hS += Y[end - 1];
+                    beg = end;
                 }
-                const bool feas = act && r == 0;
-                cnt += feas ? nLAB : 0u;
-                if (__ballot_sync(full, feas) == 0u) continue;
-                const uint64_t base = gblk + (uint64_t)(iS * nD + iD) * nLAB;
-                for (uint32_t iL = 0; iL < nL; iL++)
-                    for (uint32_t ia = 0; ia < nA; ia++) {
-                        const double *arow = alpha_tab + (size_t)ia * NT;
-                        const double aval_pp = FAM == PARADL_LAYERPURE ? dmul(lp_na, arow[ts]) : arow[ts];
-                        for (uint32_t ib = 0; ib < nB; ib++) {
-                            const double *brow = beta_tab + (size_t)ib * NT;
-                            double t = comp;
-                            if (FAM == PARADL_PD) t = dadd(t, dmul(ge_c, dadd(arow[ge_t], dmul(ge_s, brow[ge_t]))));
-                            if (FAM == PARADL_LAYERPURE)
-                                t = dadd(t, dmul(2.0, dadd(aval_pp, dmul(lp_s, brow[ts]))));
-                            else
-                                t = dadd(t, dmul(pp_c, dadd(aval_pp, dmul(pp_s, brow[ts]))));
-                            const double key = feas ? dmul(t, I) : CUDART_INF;
-                            if (__any_sync(full, key <= tk.adm))
-                                tk.offer(feas, key, base + (uint64_t)(iL * nA + ia) * nB + ib);
-                        }
-                    }
             }
+        }
+        const uint64_t gbase = v.S->offset + w.lo + (blk0 + it) * span;
+        for (uint32_t x = 0; x < (1u << kLowBits); x++) {
+            StageT st;
+            int64_t ns = 1;
+            if (act) {
+                const LowE e = lt[x];
+                const int beg = e.e_last;
+                const int64_t F = PF[c_h] - PF[beg], Bw = PB[c_h] - PB[beg], U = PU[c_h] - PU[beg];
+                const int64_t Wt = PW[c_h] - PW[beg], XY = PX[c_h] - PX[beg], BI = PI[c_h] - PI[beg];
+                st.maxF = max(max(e.F, F), hF);
+                st.maxB = max(max(e.B, Bw), hB);
+                st.maxU = max(max(e.U, U), hU);
+                st.maxW = max(max(e.W, Wt), hW);
+                st.memI = max(max(e.memI, 2 * b * XY + 2 * Wt + BI), hM);
+                st.maxY = max(e.maxY, hY);
+                st.sumY = e.sumY + hS;
+                ns = e.pop + hpop + 1;
+            }
+            eval_partition<FAM>(C, act, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
         }
         tk.refresh();
-        if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next partition (inc_part = 1)
+        if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 256
     }
 }
 
 // Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
-// with the same fp64 operations compute_mid uses.
-__device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base) {
+// with the same fp64 operations compute_mid uses, and the low-bit stage tables of mode 2.
+__device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base, LowE *low_base) {
     for (int wi = 0; wi < a.n_work; wi++) {
         const WorkItem &w = a.work[wi];
-        if (w.mode != 1) continue;
+        if (w.mode == 0) continue;
         const View v = make_view(smem, w.sub);
         const SubHdr *S = v.S;
         const uint32_t nS = S->radix[D_S], nD = S->radix[D_DIMS];
@@ -1277,11 +1416,45 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 tab[e] = ddiv(i2d(v.M->D), i2d(b * pd));
             }
         }
+        if (w.mode == 2) {
+            const ModelHdr *M = v.M;
+            const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+            const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+            const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+            const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+            const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+            const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+            const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+            const uint32_t n = S->radix[D_B] << kLowBits;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+                const uint32_t ib = e >> kLowBits, x = e & ((1u << kLowBits) - 1);
+                const int64_t b = bv[ib];
+                LowE L{};
+                int beg = 0;
+                uint32_t m = x;
+                while (m) {   // stages [beg, end) closed by low cuts
+                    const int end = __ffs(m);
+                    m &= m - 1;
+                    const int64_t Wt = PW[end] - PW[beg], XY = PX[end] - PX[beg], BI = PI[end] - PI[beg];
+                    L.F = max(L.F, PF[end] - PF[beg]);
+                    L.B = max(L.B, PB[end] - PB[beg]);
+                    L.U = max(L.U, PU[end] - PU[beg]);
+                    L.W = max(L.W, Wt);
+                    L.memI = max(L.memI, 2 * b * XY + 2 * Wt + BI);
+                    L.maxY = max(L.maxY, Y[end - 1]);
+                    L.sumY += Y[end - 1];
+                    beg = end;
+                }
+                L.e_last = beg;
+                L.pop = __popc(x);
+                (low_base + w.low_off)[e] = L;
+            }
+        }
     }
     __syncthreads();
 }
 
-template <int FAM, bool DENSE, bool BLK>
+template <int FAM, bool DENSE, int BLK>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t mbar;
@@ -1297,7 +1470,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     unsigned long long cnt = 0;
     constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
     double *memo = reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra));
-    if (BLK) build_memo(a, smem, memo);
+    LowE *lowtab = reinterpret_cast<LowE *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes);
+    if (BLK) build_memo(a, smem, memo, lowtab);
 
     for (;;) {
         unsigned long long t = 0;
@@ -1308,8 +1482,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         int wi = 0;
         while (wi + 1 < a.n_work && T >= a.work[wi + 1].tile_base) wi++;
         const WorkItem &w = a.work[wi];
-        if (BLK)
+        if (BLK == 1)
             tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo);
+        else if (BLK == 2)
+            tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
         else
             tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
     }
@@ -1692,18 +1868,21 @@ cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t 
 // ------------------------------------------------------------------ launchers
 size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
-static void *sweep_fn(int family, bool dense, bool blk) {
+static void *sweep_fn(int family, bool dense, int blk) {
     if (blk) {
         if (dense) return nullptr;
         switch (family) {
-        case PARADL_PIPELINE: return (void *)sweep_kernel<PARADL_PIPELINE, false, true>;
-        case PARADL_LAYERPURE: return (void *)sweep_kernel<PARADL_LAYERPURE, false, true>;
-        case PARADL_PD: return (void *)sweep_kernel<PARADL_PD, false, true>;
+        case PARADL_PIPELINE:
+            return blk == 1 ? (void *)sweep_kernel<PARADL_PIPELINE, false, 1> : (void *)sweep_kernel<PARADL_PIPELINE, false, 2>;
+        case PARADL_LAYERPURE:
+            return blk == 1 ? (void *)sweep_kernel<PARADL_LAYERPURE, false, 1> : (void *)sweep_kernel<PARADL_LAYERPURE, false, 2>;
+        case PARADL_PD:
+            return blk == 1 ? (void *)sweep_kernel<PARADL_PD, false, 1> : (void *)sweep_kernel<PARADL_PD, false, 2>;
         default: return nullptr;
         }
     }
 #define PARADL_CASE(F) \
-    case F: return dense ? (void *)sweep_kernel<F, true, false> : (void *)sweep_kernel<F, false, false>;
+    case F: return dense ? (void *)sweep_kernel<F, true, 0> : (void *)sweep_kernel<F, false, 0>;
     switch (family) {
         PARADL_CASE(PARADL_SERIAL)
         PARADL_CASE(PARADL_DATA)
@@ -1720,7 +1899,7 @@ static void *sweep_fn(int family, bool dense, bool blk) {
 #undef PARADL_CASE
 }
 
-int max_blocks_per_sm(int family, bool dense, bool blk, size_t smem) {
+int max_blocks_per_sm(int family, bool dense, int blk, size_t smem) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
@@ -1729,7 +1908,7 @@ int max_blocks_per_sm(int family, bool dense, bool blk, size_t smem) {
     return nb;
 }
 
-cudaError_t launch_sweep(int family, bool dense, bool blk, const LaunchArgs &a, int grid, size_t smem,
+cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, int grid, size_t smem,
                          cudaStream_t st) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return cudaErrorInvalidValue;

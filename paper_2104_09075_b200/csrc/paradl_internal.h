@@ -89,7 +89,8 @@ struct WorkItem {
                                    // (pipeline families: each lane owns whole partitions, [lo,hi) aligned)
     uint64_t inc_part;
     const HaloEntry *halo;         // spatial / ds: [n_dims][n_Ls] table (device global), else null
-    uint32_t memo_off, memo_n;     // mode 1: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
+    uint32_t memo_off, memo_n;     // mode 1/2: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
+    uint32_t low_off, pad2;        // mode 2: index of its [n_b][256] low-bit stage table (LowE units)
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
@@ -98,7 +99,7 @@ struct LaunchArgs {
     uint32_t img_bytes;            // multiple of 16
     int32_t n_work;
     uint32_t memo_bytes;           // lane-blocked memo tables after SmemExtra (multiple of 16)
-    uint32_t pad_;
+    uint32_t low_bytes;            // mode-2 low-bit stage tables after the memo tables
     uint64_t first;                // global index of dense element 0
     uint64_t total_tiles;
     int32_t shard, n_shards;
@@ -128,9 +129,9 @@ struct HaloJobs {
 // launchers implemented in kernels.cu
 cudaError_t launch_prep_model(const paradl_layer *d_rows, int32_t G, int64_t D, uint8_t *d_block,
                               const ModelHdr &layout, cudaStream_t st);
-cudaError_t launch_sweep(int family, bool dense, bool blk, const LaunchArgs &a, int grid, size_t smem,
+cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, int grid, size_t smem,
                          cudaStream_t st);
-int max_blocks_per_sm(int family, bool dense, bool blk, size_t smem);
+int max_blocks_per_sm(int family, bool dense, int blk, size_t smem);
 size_t sweep_smem_extra();
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,

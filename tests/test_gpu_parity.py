@@ -258,3 +258,32 @@ def test_sharded_topk_merge_equals_single(dev, oracle_mod):
         got = [int(v) for v in o[:, 0].astype(np.uint64)]
         assert got == [h[0] for h in single]
         assert int(cnt.item()) == nf
+
+
+@pytest.mark.parametrize("seed,G,fam", [(11, 10, W.PIPELINE), (12, 12, W.PD), (13, 13, W.LAYERPURE),
+                                         (14, 11, W.PD), (15, 14, W.PIPELINE)])
+def test_lane_blocked_modes(dev, oracle_mod, seed, G, fam):
+    """Lane-blocked evaluation (COMB partitions and 256-mask blocks with the low-bit stage
+    table) against the oracle on whole sweeps and ragged sub-ranges."""
+    m = corpus.random_model(seed, G=G)
+    sysd = corpus.random_system(seed)
+    nt = len(sysd.tiers)
+    A = [[1e-6 * (i + 1) * (t + 1) for t in range(nt)] for i in range(2)]
+    Bt = [[1e-10 * (i + 3) * (t + 1) for t in range(nt)] for i in range(3)]
+    common = dict(b=[2, 8], S=[1, 2, 4], alpha=A, beta=Bt, cap=[2.0 ** 20, 2.0 ** 40])
+    if fam == W.PD:
+        common["dims"] = [(p, 1, 1, 1) for p in (1, 2, 8)]
+    subs = [W.SubSweep(fam, part_mode=W.PART_MASK, **common),
+            W.SubSweep(fam, part_mode=W.PART_COMB, s_min=1, s_max=min(4, G), **common)]
+    sw = W.Sweep([m], sysd, subs, "blocked")
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    for k in (1, 64):
+        check_topk(ctx, spec, osw, 0, n, k)
+    rng = random.Random(seed)
+    for _ in range(4):
+        a = rng.randrange(n)
+        c = rng.randrange(1, n - a + 1)
+        check_topk(ctx, spec, osw, a, c, rng.choice([3, 33]))
