@@ -712,8 +712,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 w.steps = (uint32_t)cper;
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
             } else {
-                // >= ~8 tiles per warp for balance, 32..32768 configurations per tile
-                uint64_t steps = range / (32ull * warps * 8ull);
+                // >= ~8 tiles per warp for balance, but at least one whole alpha/beta block per
+                // tile (structure terms are computed once per block), 32..32768 configs per tile
+                const SubHdr &h = P.subs[w.sub].hdr;
+                const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
+                uint64_t steps = std::max<uint64_t>(range / (32ull * warps * 8ull), (nAB + 31) / 32);
                 steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
                 w.steps = (uint32_t)steps;
                 w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
@@ -723,7 +726,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         }
         a.total_tiles = tiles;
         const uint64_t my_tiles = tiles > (uint64_t)shard ? (tiles - shard + n_shards - 1) / n_shards : 0;
-        const uint64_t need_ctas = (my_tiles + 4ull * kWarps - 1) / (4ull * kWarps);   // >= 4 tiles per warp
+        const uint64_t need_ctas = (my_tiles + kWarps - 1) / kWarps;   // small launches: one tile per warp
         grids[li] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid_max, need_ctas));
         total_ctas += grids[li];
     }

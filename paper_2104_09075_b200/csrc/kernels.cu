@@ -952,7 +952,9 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
     const uint32_t nB = v.S->radix[D_BETA];
     const uint32_t nAB = v.S->radix[D_ALPHA] * nB;     // host guarantees < 2^31
     const uint32_t dB = 32u % nB, dA = 32u / nB;        // lane stride 32 inside the alpha/beta block
-    const bool slots = (nB == 32u || nB == 64u);        // beta-slot caching applies (M = nB / 32)
+    // beta-slot caching (M = nB / 32) needs every lane of a step in the same 32-aligned beta
+    // window, i.e. a 32-aligned range start (tile starts are lo + multiples of 32)
+    const bool slots = (nB == 32u || nB == 64u) && (w.lo & 31u) == 0;
     const bool M2 = nB == 64u;
     const unsigned full = 0xffffffffu;
         const uint64_t u0 = w.lo + tile * TS;

@@ -287,3 +287,18 @@ def test_lane_blocked_modes(dev, oracle_mod, seed, G, fam):
         a = rng.randrange(n)
         c = rng.randrange(1, n - a + 1)
         check_topk(ctx, spec, osw, a, c, rng.choice([3, 33]))
+
+
+def test_unaligned_windows_all_families(dev, oracle_mod):
+    """Ranges starting at every residue mod 32 (lane/slot alignment edge cases), cfg2 shapes."""
+    sw = W.config2(n_alpha=3, n_beta=64, b_list=[2, 64], pipe_smax=2)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    rng = random.Random(7)
+    for r in range(32):
+        a = rng.randrange(n // 32 - 200) * 32 + r
+        c = rng.choice([31, 32, 33, 700, 5000])
+        check_topk(ctx, spec, osw, a, c, 5)
+        check_dense(ctx, spec, osw, a, c, dev)
