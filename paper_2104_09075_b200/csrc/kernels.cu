@@ -849,9 +849,13 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
         r = 1;
         a++;
     }
-    // R = 4/M whole alpha rows per iteration: 4 independent dependency chains; the
-    // admission test is one ballot per key (no min/select sequence)
-    constexpr int R = 4 / M;
+    // R = KEYS/M whole alpha rows per iteration: KEYS independent dependency chains (16 for
+    // the light families, 8 where more comm terms would spill); the admission test is one
+    // ballot per key (no min/select sequence)
+    constexpr int KEYS = (FAM == PARADL_PIPELINE || FAM == PARADL_DATA || FAM == PARADL_LAYERPURE) ? 16
+                         : (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_DF)        ? 4
+                                                                                                  : 8;
+    constexpr int R = KEYS / M;
     const double *ap = alpha_tab + (size_t)a * NT;
     while (r + R * M <= run) {
         double key[R * M];
