@@ -14,7 +14,7 @@ import os
 from . import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparadl.so")
+LIB_PATH = os.environ.get("PARADL_LIB") or os.path.join(HERE, "libparadl.so")   # override: experiments only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

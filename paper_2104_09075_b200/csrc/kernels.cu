@@ -677,18 +677,24 @@ struct WarpTopK {
     // non-negative double (monotone as uint64) under atomicMin; ~0 = none yet.
     double adm;
     unsigned long long *gbound;
+    unsigned long long gnext;   // bound loaded at the previous refresh (software-pipelined load)
 
     __device__ void init(int kk, unsigned long long *g = nullptr) {
         k = kk;
         ka = kb = thk = adm = CUDART_INF;
         ia = ib = thi = ~0ull;
         gbound = g;
+        gnext = ~0ull;
     }
-    // re-read the shared bound (whole warp; cheap broadcast load)
+    // adopt the shared bound loaded at the previous call and issue the next load, so the
+    // global-memory latency overlaps the work in between (whole warp; broadcast load)
+    // (blocking while this warp has no bound at all, e.g. short-lived warps of small launches)
     __device__ __forceinline__ void refresh() {
         if (!gbound) return;
-        const unsigned long long g = *(volatile unsigned long long *)gbound;
-        if (g != ~0ull) adm = fmin(thk, __longlong_as_double((long long)g));
+        unsigned long long g = gnext;
+        if (adm == CUDART_INF) g = *(volatile unsigned long long *)gbound;
+        gnext = *(volatile unsigned long long *)gbound;
+        if (g != ~0ull) adm = fmin(adm, fmin(thk, __longlong_as_double((long long)g)));
     }
     // after thk changed: tighten adm and publish a full list's threshold
     __device__ __forceinline__ void publish() {
