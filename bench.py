@@ -201,8 +201,9 @@ def ours(args):
 
     lists = torch.empty((max(ws, 1), K_TOP, 2), dtype=torch.int64, device=dev)
     counts = torch.zeros(max(ws, 1), dtype=torch.int64, device=dev)
-    my_hits = torch.empty((K_TOP, 2), dtype=torch.int64, device=dev)
-    my_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    my_rec = torch.zeros((K_TOP + 1, 2), dtype=torch.int64, device=dev)   # k hits + count record
+    my_hits = my_rec[:K_TOP]
+    my_cnt = my_rec[K_TOP, :1]
     out = torch.empty((K_TOP, 2), dtype=torch.int64, device=dev)
     out_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -213,7 +214,7 @@ def ours(args):
 
     def step():
         if ws > 1:
-            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_hits, my_cnt, stream=stream)
+            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_rec, stream=stream)
             launches[0] += st_["launches"]
             return out, out_cnt
         ctx.topk_async(spec, 0, N, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
@@ -276,7 +277,7 @@ def ours(args):
             dist.barrier()
             t0 = time.perf_counter()
             ctx.set_system(sweep.system)
-            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_hits, my_cnt, stream=stream)
+            _, _, st_ = PD.sharded_topk(ctx, spec, 0, N, K_TOP, out, out_cnt, my_rec, stream=stream)
             h2d = st_["h2d"]
             host = out.cpu()
             _ = out_cnt.cpu()

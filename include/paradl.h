@@ -205,6 +205,13 @@ paradl_status paradl_merge_topk(paradl_ctx *ctx, const paradl_hit *d_lists, int3
                                 int32_t k, const uint64_t *d_counts, paradl_hit *d_out,
                                 uint64_t *d_count_out, void *stream);
 
+/* Multi-GPU record layout: a record is paradl_hit[k + 1] whose first k entries are a top-k
+ * list (as written by paradl_topk_async to d_hits = record) and whose entry k holds the
+ * feasible count in its idx field (d_n_feasible = &record[k].idx).  Merges n_records such
+ * records (contiguous, DEVICE, e.g. one all_gather of every rank's record) asynchronously. */
+paradl_status paradl_merge_records(paradl_ctx *ctx, const paradl_hit *d_records, int32_t n_records,
+                                   int32_t k, paradl_hit *d_out, uint64_t *d_count_out, void *stream);
+
 /* Decode / explain one index (evaluated by a CUDA kernel; host outputs; synchronous). */
 paradl_status paradl_decode(paradl_ctx *ctx, const paradl_sweep_spec *spec, uint64_t idx,
                             paradl_config *out);

@@ -177,6 +177,11 @@ class Context:
         self._check(_lib.paradl_merge_topk(self._h, C.c_void_p(d_lists_ptr), n_lists, k, C.c_void_p(d_counts_ptr),
                                            C.c_void_p(d_out_ptr), C.c_void_p(d_count_out_ptr), _stream(stream)))
 
+    def merge_records(self, d_records_ptr: int, n_records: int, k: int, d_out_ptr: int, d_count_out_ptr: int,
+                      stream=None):
+        self._check(_lib.paradl_merge_records(self._h, C.c_void_p(d_records_ptr), n_records, k,
+                                              C.c_void_p(d_out_ptr), C.c_void_p(d_count_out_ptr), _stream(stream)))
+
     def sweep_dense(self, spec: Spec, first: int, count: int, t_iter_ptr=0, mem_ptr=0, bits_ptr=0, reason_ptr=0,
                     stream=None):
         out = A.DenseOut(t_iter_ptr or None, mem_ptr or None, bits_ptr or None, reason_ptr or None)

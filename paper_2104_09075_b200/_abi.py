@@ -86,7 +86,7 @@ STRUCTS = [Layer, System, SubSweep, Config, Prediction, Hit]
 EXPORTS = ["paradl_create", "paradl_destroy", "paradl_last_error", "paradl_version", "paradl_load_model",
            "paradl_set_system", "paradl_sweep_size", "paradl_sweep", "paradl_topk", "paradl_argmin",
            "paradl_topk_async", "paradl_merge_topk", "paradl_decode", "paradl_explain", "paradl_struct_size",
-           "paradl_stat", "paradl_fp64_peak"]
+           "paradl_stat", "paradl_fp64_peak", "paradl_merge_records"]
 
 
 def declare(lib):
@@ -107,6 +107,7 @@ def declare(lib):
     lib.paradl_topk_async.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32,
                                       vp, vp, vp]
     lib.paradl_merge_topk.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
+    lib.paradl_merge_records.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp]
     lib.paradl_decode.argtypes = [vp, P(SweepSpec), C.c_uint64, P(Config)]
     lib.paradl_explain.argtypes = [vp, P(SweepSpec), C.c_uint64, P(Prediction)]
     lib.paradl_stat.argtypes = [vp, C.c_int32]

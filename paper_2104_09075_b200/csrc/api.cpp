@@ -69,6 +69,13 @@ struct paradl_ctx {
     std::vector<cudaEvent_t> events;
     cudaEvent_t fork_ev = nullptr;
     unsigned long long *last_count_ptr = nullptr;
+    uint64_t sys_epoch = 0;
+    // plan cache: serialized spec of the last planned sweep and its plan (host-side only)
+    std::vector<uint8_t> plan_key;
+    uint64_t plan_sys_epoch = ~0ull, plan_models_epoch = ~0ull;
+    void *plan_cached = nullptr;   // Plan*
+    // occupancy / smem-attribute cache: (family, dense, blk, smem) -> blocks per SM
+    std::vector<std::pair<uint64_t, int>> occ_cache;
     uint64_t models_epoch = 0, img_epoch = ~0ull;
 };
 
@@ -117,6 +124,8 @@ extern "C" paradl_status paradl_create(int32_t cuda_device, paradl_ctx **out) {
     return PARADL_OK;
 }
 
+static void free_plan(void *p);
+
 extern "C" void paradl_destroy(paradl_ctx *c) {
     if (!c) return;
     if (c->device >= 0) {
@@ -133,6 +142,7 @@ extern "C" void paradl_destroy(paradl_ctx *c) {
         for (auto e2 : c->events) cudaEventDestroy(e2);
         if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     }
+    free_plan(c->plan_cached);
     delete c;
 }
 
@@ -261,6 +271,7 @@ extern "C" paradl_status paradl_set_system(paradl_ctx *c, const paradl_system *s
     c->sys = *s;
     c->have_system = true;
     c->img_epoch = ~0ull;
+    c->sys_epoch++;
     return PARADL_OK;
 }
 
@@ -290,7 +301,7 @@ uint64_t binom_u64(int64_t n, int64_t k) {
 
 }  // namespace
 
-static paradl_status plan_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, Plan &P) {
+static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *spec, Plan &P) {
     if (!spec || spec->n_sub < 1 || !spec->sub) return fail(c, PARADL_EINVAL, "empty sweep spec");
     if (spec->n_sub > kMaxSub) return fail(c, PARADL_EINVAL, "at most %d sub-sweeps", kMaxSub);
     if (!c->have_system) return fail(c, PARADL_ESTATE, "paradl_set_system not called");
@@ -499,6 +510,62 @@ static paradl_status plan_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, Pl
     return PARADL_OK;
 }
 
+static void free_plan(void *p) { delete (Plan *)p; }
+
+// Serialises every input a plan depends on (spec fields and list contents).
+static void spec_key(const paradl_sweep_spec *spec, int NT, std::vector<uint8_t> &k) {
+    k.clear();
+    auto app = [&](const void *p, size_t n) {
+        const uint8_t *b = (const uint8_t *)p;
+        k.insert(k.end(), b, b + n);
+    };
+    app(&spec->n_sub, sizeof spec->n_sub);
+    for (int i = 0; i < spec->n_sub; i++) {
+        const paradl_subsweep &x = spec->sub[i];
+        app(&x.family, 14 * sizeof(int32_t));   // family .. reserved (scalar header)
+        if (x.n_cap > 0 && x.cap) app(x.cap, 8ull * x.n_cap);
+        if (x.n_flops > 0 && x.flops) app(x.flops, 8ull * x.n_flops);
+        if (x.n_b > 0 && x.b) app(x.b, 8ull * x.n_b);
+        if (x.n_S > 0 && x.S) app(x.S, 4ull * x.n_S);
+        if (x.n_dims > 0 && x.dims) app(x.dims, 16ull * x.n_dims);
+        if (x.n_Ls > 0 && x.Ls) app(x.Ls, 4ull * x.n_Ls);
+        if (x.n_alpha > 0 && x.alpha) app(x.alpha, 8ull * x.n_alpha * NT);
+        if (x.n_beta > 0 && x.beta) app(x.beta, 8ull * x.n_beta * NT);
+    }
+}
+
+// Plans the sweep into the ctx-owned plan, reusing it when the spec, system and models are
+// unchanged (the bench and multi-GPU steps call the same sweep repeatedly).  *out stays
+// valid until the next planning call on this ctx.
+static paradl_status plan_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, const Plan **out) {
+    Plan *cached = (Plan *)c->plan_cached;
+    if (!cached) {
+        cached = new (std::nothrow) Plan();
+        if (!cached) return fail(c, PARADL_ENOMEM, "out of host memory");
+        c->plan_cached = cached;
+    }
+    std::vector<uint8_t> key;
+    const bool keyable = spec && spec->n_sub >= 1 && spec->sub && spec->n_sub <= kMaxSub && c->have_system;
+    if (keyable) {
+        spec_key(spec, c->sys.n_tiers, key);
+        if (c->plan_sys_epoch == c->sys_epoch && c->plan_models_epoch == c->models_epoch && key == c->plan_key) {
+            *out = cached;
+            return PARADL_OK;
+        }
+    }
+    c->plan_sys_epoch = ~0ull;   // invalid until rebuilt successfully
+    *cached = Plan();
+    paradl_status st = plan_sweep_build(c, spec, *cached);
+    if (st) return st;
+    if (keyable) {
+        c->plan_key.swap(key);
+        c->plan_sys_epoch = c->sys_epoch;
+        c->plan_models_epoch = c->models_epoch;
+    }
+    *out = cached;
+    return PARADL_OK;
+}
+
 static paradl_status need_device(paradl_ctx *c) {
     if (!c) return PARADL_EINVAL;
     c->stat_h2d = c->stat_d2h = c->stat_launches = 0;
@@ -530,9 +597,10 @@ static paradl_status upload(paradl_ctx *c, const Plan &P, cudaStream_t st) {
 
 extern "C" paradl_status paradl_sweep_size(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t *n) {
     if (!c || !n) return PARADL_EINVAL;
-    Plan P;
-    paradl_status st = plan_sweep(c, spec, P);
+    const Plan *PP = nullptr;
+    paradl_status st = plan_sweep(c, spec, &PP);
     if (st) return st;
+    const Plan &P = *PP;
     *n = P.total;
     return PARADL_OK;
 }
@@ -575,7 +643,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         if (r0 >= r1) continue;
         const int fam = P.subs[q].family;
         size_t li = 0;
-        while (li < fam_of.size() && fam_of[li] != fam) li++;
+        while (li < fam_of.size() && (fam_of[li] != fam || L[li].n_work + 3 > kMaxWork)) li++;
         if (li == fam_of.size()) {
             fam_of.push_back(fam);
             L.emplace_back();
@@ -590,7 +658,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         const uint64_t Q = nAB * h.radix[D_LS] * h.radix[D_DIMS] * h.radix[D_S];
         const uint64_t memo_n = (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]);
         const bool mask2 = h.part_mode == PARADL_PART_MASK && h.G >= 10 && h.radix[D_B] <= 2;
-        const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22) && a.n_work + 3 <= kMaxSub)
+        const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22))
                              ? (mask2 ? 2 : 1)
                              : 0;
         const uint64_t unit = mode == 2 ? Q << 8 : Q;
@@ -693,7 +761,15 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
         smems[li] = smem + a.memo_bytes + a.low_bytes;
-        const int nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li], smems[li]);
+        const uint64_t okey = ((uint64_t)fam_of[li] << 40) | ((uint64_t)dense << 39) | ((uint64_t)blk_of[li] << 36) |
+                              (uint64_t)smems[li];
+        int nb = -1;
+        for (auto &kv : c->occ_cache)
+            if (kv.first == okey) nb = kv.second;
+        if (nb < 0) {
+            nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li], smems[li]);
+            c->occ_cache.push_back({okey, nb});
+        }
         if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smems[li]);
         const int grid_max = c->n_sm * nb;
         const uint64_t warps = (uint64_t)grid_max * kWarps;
@@ -706,8 +782,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
                 const uint64_t nblk = range / (w.mode == 2 ? Q << 8 : Q);
-                // >= ~8 tiles per warp; 1..256 partitions per lane per tile
-                uint64_t cper = nblk / (32ull * warps * 8ull);
+                // >= ~8 tiles per warp of this rank's shard; 1..256 partitions per lane per tile
+                uint64_t cper = nblk / n_shards / (32ull * warps * 8ull);
                 cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
                 w.steps = (uint32_t)cper;
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
@@ -716,7 +792,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 // tile (structure terms are computed once per block), 32..32768 configs per tile
                 const SubHdr &h = P.subs[w.sub].hdr;
                 const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
-                uint64_t steps = std::max<uint64_t>(range / (32ull * warps * 8ull), (nAB + 31) / 32);
+                uint64_t steps = std::max<uint64_t>(range / n_shards / (32ull * warps * 8ull), (nAB + 31) / 32);
                 steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 1024));
                 w.steps = (uint32_t)steps;
                 w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
@@ -735,6 +811,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     unsigned long long *ctr = (unsigned long long *)c->counters.p;
     CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
     CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
+
     if (halo_entries) {
         CUDA_TRY(c, launch_halo_tables(hj, st));
         c->stat_launches++;
@@ -794,9 +871,10 @@ extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *sp
     paradl_status s = need_device(c);
     if (s) return s;
     if (!out) return fail(c, PARADL_EINVAL, "null dense output");
-    Plan P;
-    s = plan_sweep(c, spec, P);
+    const Plan *PP = nullptr;
+    s = plan_sweep(c, spec, &PP);
     if (s) return s;
+    const Plan &P = *PP;
     if (first > P.total || count > P.total - first) return fail(c, PARADL_ERANGE, "range outside the sweep (%llu configs)", (unsigned long long)P.total);
     cudaStream_t st = (cudaStream_t)stream;
     s = upload(c, P, st);
@@ -814,9 +892,10 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
     if (k < 1 || k > PARADL_MAX_TOPK) return fail(c, PARADL_EINVAL, "k must be in 1..%d", PARADL_MAX_TOPK);
     if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(c, PARADL_EINVAL, "bad shard / n_shards");
     if (!d_hits || !d_n_feasible) return fail(c, PARADL_EINVAL, "null output");
-    Plan P;
-    s = plan_sweep(c, spec, P);
+    const Plan *PP = nullptr;
+    s = plan_sweep(c, spec, &PP);
     if (s) return s;
+    const Plan &P = *PP;
     if (first > P.total || count > P.total - first) return fail(c, PARADL_ERANGE, "range outside the sweep (%llu configs)", (unsigned long long)P.total);
     cudaStream_t st = (cudaStream_t)stream;
     s = upload(c, P, st);
@@ -832,7 +911,7 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
         CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     }
     CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
-                             (unsigned long long *)d_n_feasible, st));
+                             (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr));
     c->stat_launches++;
     return PARADL_OK;
 }
@@ -846,6 +925,19 @@ extern "C" paradl_status paradl_merge_topk(paradl_ctx *c, const paradl_hit *d_li
         return fail(c, PARADL_EINVAL, "bad merge arguments");
     CUDA_TRY(c, launch_merge(d_lists, n_lists, k, (const unsigned long long *)d_counts, n_lists, d_out,
                              (unsigned long long *)d_count_out, (cudaStream_t)stream));
+    c->stat_launches++;
+    return PARADL_OK;
+}
+
+extern "C" paradl_status paradl_merge_records(paradl_ctx *c, const paradl_hit *d_records, int32_t n_records,
+                                              int32_t k, paradl_hit *d_out, uint64_t *d_count_out, void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (k < 1 || k > PARADL_MAX_TOPK || n_records < 0 || (n_records && !d_records) || !d_out || !d_count_out)
+        return fail(c, PARADL_EINVAL, "bad merge arguments");
+    const unsigned long long *counts = n_records ? (const unsigned long long *)&d_records[k].idx : nullptr;
+    CUDA_TRY(c, launch_merge(d_records, n_records, k, counts, n_records, d_out, (unsigned long long *)d_count_out,
+                             (cudaStream_t)stream, nullptr, k + 1, (int32_t)((k + 1) * sizeof(paradl_hit) / 8)));
     c->stat_launches++;
     return PARADL_OK;
 }
@@ -878,9 +970,10 @@ static paradl_status explain_impl(paradl_ctx *c, const paradl_sweep_spec *spec, 
                                   paradl_prediction *pred) {
     paradl_status s = need_device(c);
     if (s) return s;
-    Plan P;
-    s = plan_sweep(c, spec, P);
+    const Plan *PP = nullptr;
+    s = plan_sweep(c, spec, &PP);
     if (s) return s;
+    const Plan &P = *PP;
     if (idx >= P.total) return fail(c, PARADL_ERANGE, "index %llu outside the sweep", (unsigned long long)idx);
     s = upload(c, P, 0);
     if (s) return s;

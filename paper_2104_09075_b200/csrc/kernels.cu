@@ -16,6 +16,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "paradl_internal.h"
 
 namespace paradl {
@@ -1535,7 +1537,9 @@ __device__ __forceinline__ void hit_min(double &k, uint64_t &i, double k2, uint6
 
 __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, int64_t n_lists, int32_t k,
                                                       const unsigned long long *counts, int32_t n_counts,
-                                                      paradl_hit *out, unsigned long long *count_out) {
+                                                      paradl_hit *out, unsigned long long *count_out,
+                                                      const unsigned long long *gbound, int32_t lstride,
+                                                      int32_t cstride, unsigned long long *bound_out) {
     __shared__ paradl_hit cand[kMergeCand];
     __shared__ unsigned long long s_cnt;
     __shared__ double s_wk[32];
@@ -1549,12 +1553,13 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     }
     __syncthreads();
     unsigned long long c = 0;
-    for (int i = threadIdx.x; i < n_counts; i += blockDim.x) c += counts[i];
+    for (int i = threadIdx.x; i < n_counts; i += blockDim.x) c += counts[(int64_t)i * cstride];
     atomicAdd(&s_cnt, c);
     // 1. bound: smallest k-th entry over the lists
     double bk = CUDART_INF;
     uint64_t bi = ~0ull;
-    for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) hit_min(bk, bi, lists[l * k + (k - 1)].key_epoch_s, lists[l * k + (k - 1)].idx);
+    for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x)
+        hit_min(bk, bi, lists[l * lstride + (k - 1)].key_epoch_s, lists[l * lstride + (k - 1)].idx);
     for (int o = 16; o; o >>= 1) hit_min(bk, bi, __shfl_xor_sync(full, bk, o), __shfl_xor_sync(full, bi, o));
     if (lane == 0) {
         s_wk[warp] = bk;
@@ -1573,14 +1578,21 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     __syncthreads();
     bk = s_wk[0];
     bi = s_wi[0];
-    // 2. candidates <= bound (sorted lists: stop at the first larger entry)
-    for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
-        for (int j = 0; j < k; j++) {
-            const paradl_hit h = lists[l * k + j];
-            if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) break;
-            const int pos = atomicAdd(&s_nc, 1);
-            if (pos < kMergeCand) cand[pos] = h;
-        }
+    // the sweep's shared admission bound (any warp's k-th key) is also valid: keys above it
+    // cannot be in the top k (key-only bound: ties at it stay candidates)
+    if (gbound) {
+        const unsigned long long g = *gbound;
+        if (g != ~0ull) hit_min(bk, bi, __longlong_as_double((long long)g), ~0ull);
+    }
+    // 2. candidates <= bound: one thread per entry (independent, coalesced loads; a per-list
+    //    walk would chain one global-memory latency per entry)
+    const int64_t n_ent = n_lists * (int64_t)k;
+    for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
+        const int64_t l = e / k, j = e - l * k;
+        const paradl_hit h = lists[l * lstride + j];
+        if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
+        const int pos = atomicAdd(&s_nc, 1);
+        if (pos < kMergeCand) cand[pos] = h;
     }
     __syncthreads();
     const int nc = s_nc;
@@ -1594,8 +1606,13 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
         }
         __syncthreads();
         bitonic_sort_smem(cand, n2);
-        for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = cand[i];
-        if (threadIdx.x == 0) *count_out = s_cnt;
+        if (out)
+            for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = cand[i];
+        if (threadIdx.x == 0) {
+            if (count_out) *count_out = s_cnt;
+            if (bound_out && cand[k - 1].idx != ~0ull)
+                atomicMin(bound_out, (unsigned long long)__double_as_longlong(cand[k - 1].key_epoch_s));
+        }
         return;
     }
     if (warp != 0) return;
@@ -1606,19 +1623,22 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
         const int64_t n = n_lists * (int64_t)k;
         for (int64_t e = 0; e < n; e += 32) {
             const int64_t j = e + lane;
-            const bool ok = j < n && lists[j].idx != ~0ull;
-            tk.offer(ok, ok ? lists[j].key_epoch_s : CUDART_INF, ok ? lists[j].idx : ~0ull);
+            const int64_t jj = (j / k) * lstride + (j % k);
+            const bool ok = j < n && lists[jj].idx != ~0ull;
+            tk.offer(ok, ok ? lists[jj].key_epoch_s : CUDART_INF, ok ? lists[jj].idx : ~0ull);
         }
     }
-    if (lane < k) {
+    if (out && lane < k) {
         out[lane].idx = tk.ia;
         out[lane].key_epoch_s = tk.ka;
     }
-    if (lane + 32 < k) {
+    if (out && lane + 32 < k) {
         out[lane + 32].idx = tk.ib;
         out[lane + 32].key_epoch_s = tk.kb;
     }
-    if (lane == 0) *count_out = s_cnt;
+    if (lane == 0 && count_out) *count_out = s_cnt;
+    if (bound_out && tk.thi != ~0ull && lane == 0)
+        atomicMin(bound_out, (unsigned long long)__double_as_longlong(tk.thk));
 }
 
 // ------------------------------------------------------------------ explain / decode
@@ -1911,10 +1931,31 @@ static void *sweep_fn(int family, bool dense, int blk) {
 #undef PARADL_CASE
 }
 
+// The max-dynamic-smem attribute is per function and process-wide: only ever raise it, so a
+// query for a small launch cannot invalidate a later launch that needs more.
+static cudaError_t ensure_smem_attr(void *fn, size_t smem) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static struct {
+        void *fn;
+        size_t smem;
+    } cache[64];
+    static int n = 0;
+    int slot = -1;
+    for (int i = 0; i < n; i++)
+        if (cache[i].fn == fn) slot = i;
+    if (slot >= 0 && cache[slot].smem >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (slot < 0 && n < 64) slot = n++;
+    if (slot >= 0) cache[slot] = {fn, smem};
+    return cudaSuccess;
+}
+
 int max_blocks_per_sm(int family, bool dense, int blk, size_t smem) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return 0;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (ensure_smem_attr(fn, smem) != cudaSuccess) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) return 0;
     return nb;
@@ -1924,15 +1965,18 @@ cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, i
                          cudaStream_t st) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem_attr(fn, smem);
     if (e != cudaSuccess) return e;
     void *args[] = {const_cast<LaunchArgs *>(&a)};
     return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k, const unsigned long long *counts,
-                         int32_t n_counts, paradl_hit *out, unsigned long long *count_out, cudaStream_t st) {
-    merge_kernel<<<1, 1024, 0, st>>>(lists, n_lists, k, counts, n_counts, out, count_out);
+                         int32_t n_counts, paradl_hit *out, unsigned long long *count_out, cudaStream_t st,
+                         const unsigned long long *gbound, int32_t lstride, int32_t cstride,
+                         unsigned long long *bound_out) {
+    merge_kernel<<<1, 1024, 0, st>>>(lists, n_lists, k, counts, n_counts, out, count_out, gbound,
+                                     lstride > 0 ? lstride : k, cstride > 0 ? cstride : 1, bound_out);
     return cudaGetLastError();
 }
 

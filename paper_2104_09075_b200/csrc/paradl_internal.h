@@ -18,6 +18,7 @@
 namespace paradl {
 
 constexpr int kMaxSub = 64;
+constexpr int kMaxWork = 8;              // work items per sweep launch (kernel parameter size)
 constexpr int kMaxModelsPerSweep = 8;
 constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
@@ -112,7 +113,7 @@ struct LaunchArgs {
     double *mem;
     uint32_t *bits;
     uint8_t *reason;
-    WorkItem work[kMaxSub];
+    WorkItem work[kMaxWork];
 };
 
 struct HaloJob {
@@ -135,7 +136,9 @@ int max_blocks_per_sm(int family, bool dense, int blk, size_t smem);
 size_t sweep_smem_extra();
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
-                         unsigned long long *count_out, cudaStream_t st);
+                         unsigned long long *count_out, cudaStream_t st,
+                         const unsigned long long *gbound = nullptr, int32_t lstride = 0, int32_t cstride = 0,
+                         unsigned long long *bound_out = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
 cudaError_t launch_explain(const uint8_t *img, uint32_t img_bytes, int32_t sub, uint64_t local,

@@ -29,17 +29,21 @@ def gather_topk(hits: torch.Tensor, count: torch.Tensor, group=None):
 
 
 def sharded_topk(ctx, spec, first: int, count: int, k: int, out_hits: torch.Tensor, out_count: torch.Tensor,
-                 my_hits: torch.Tensor, my_count: torch.Tensor, group=None, stream=None):
-    """One multi-GPU top-k step on the current device: shard -> all_gather -> device merge.
-    All tensors are int64 on the ctx's device: out_hits/my_hits [k, 2], out_count/my_count [1].
-    Returns (out_hits, out_count, stats) with this rank's H2D bytes and kernel launches."""
+                 my_rec: torch.Tensor, group=None, stream=None):
+    """One multi-GPU top-k step on the current device: shard -> one all_gather -> device merge.
+    my_rec: int64 [k + 1, 2] record (k hits, then the count in row k, column 0); out_hits
+    [k, 2] and out_count [1] int64 on the ctx's device.  Returns (out_hits, out_count, stats)
+    with this rank's H2D bytes and kernel launches."""
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    ctx.topk_async(spec, first, count, rank, ws, k, my_hits.data_ptr(), my_count.data_ptr(), stream=stream)
+    ctx.topk_async(spec, first, count, rank, ws, k, my_rec.data_ptr(), my_rec[k].data_ptr(), stream=stream)
     stats = {"h2d": ctx.stat(0), "launches": ctx.stat(2) + 1}
-    lists, counts = gather_topk(my_hits, my_count, group)
-    ctx.merge_topk(lists.data_ptr(), ws, k, counts.data_ptr(), out_hits.data_ptr(), out_count.data_ptr(),
-                   stream=stream)
+    recs = torch.empty((ws, k + 1, 2), dtype=torch.int64, device=my_rec.device)
+    if dist.get_backend(group) == "gloo":
+        dist.all_gather(list(recs.unbind(0)), my_rec.contiguous(), group=group)
+    else:
+        dist.all_gather_into_tensor(recs.view(ws, -1), my_rec.reshape(-1).contiguous(), group=group)
+    ctx.merge_records(recs.data_ptr(), ws, k, out_hits.data_ptr(), out_count.data_ptr(), stream=stream)
     return out_hits, out_count, stats
 
 

@@ -302,3 +302,26 @@ def test_unaligned_windows_all_families(dev, oracle_mod):
         c = rng.choice([31, 32, 33, 700, 5000])
         check_topk(ctx, spec, osw, a, c, 5)
         check_dense(ctx, spec, osw, a, c, dev)
+
+
+def test_merge_records_equals_single(dev):
+    """Multi-GPU record layout (k hits + count) merged by paradl_merge_records, shards
+    simulated on one GPU, equals the unsharded top-k and count."""
+    sw = W.config2(n_alpha=8, n_beta=64, b_list=[2, 32], pipe_smax=3)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    n = ctx.sweep_size(spec)
+    k = 64
+    single, nf = ctx.topk(spec, k)
+    for ns in (2, 3, 8):
+        recs = torch.zeros((ns, k + 1, 2), dtype=torch.int64, device=dev)
+        for s in range(ns):
+            ctx.topk_async(spec, 0, n, s, ns, k, recs[s].data_ptr(), recs[s, k].data_ptr(),
+                           stream=torch.cuda.current_stream())
+        out = torch.empty((k, 2), dtype=torch.int64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        ctx.merge_records(recs.data_ptr(), ns, k, out.data_ptr(), cnt.data_ptr(), stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        got = [int(v) for v in out.cpu().numpy()[:, 0].astype(np.uint64)]
+        assert got == [h[0] for h in single]
+        assert int(cnt.item()) == nf
