@@ -810,11 +810,18 @@ struct WarpTopK {
         }
         publish();
     }
-    // whole warp; per-lane candidate (valid, key, idx)
-    __device__ __forceinline__ void offer(bool valid, double key, uint64_t idx) {
+    // whole warp; per-lane candidate (valid, key, idx).  The insertion code is large, so it
+    // lives in one out-of-line function (state passed by value) instead of being inlined at
+    // every call site: short-lived launches are otherwise instruction-cache bound.
+    __device__ __forceinline__ void offer(bool valid, double key, uint64_t idx);
+    // inline variant for call sites that are few (lane-blocked inner loops)
+    __device__ __forceinline__ void offer_inl(bool valid, double key, uint64_t idx) {
+        const bool cand = valid && key <= adm && key <= thk && (key < thk || idx < thi);
+        const unsigned msk = __ballot_sync(0xffffffffu, cand);
+        if (msk) offer_slow(cand, msk, key, idx);
+    }
+    __device__ __forceinline__ void offer_slow(bool cand, unsigned msk, double key, uint64_t idx) {
         const unsigned full = 0xffffffffu;
-        bool cand = valid && key <= adm && key <= thk && (key < thk || idx < thi);
-        unsigned msk = __ballot_sync(full, cand);
         if (__popc(msk) >= 6) {
             batch(cand ? key : CUDART_INF, cand ? idx : ~0ull);
             return;
@@ -828,6 +835,17 @@ struct WarpTopK {
         }
     }
 };
+
+__device__ __noinline__ WarpTopK topk_offer_slow(WarpTopK t, bool cand, unsigned msk, double key, uint64_t idx) {
+    t.offer_slow(cand, msk, key, idx);
+    return t;
+}
+
+__device__ __forceinline__ void WarpTopK::offer(bool valid, double key, uint64_t idx) {
+    const bool cand = valid && key <= adm && key <= thk && (key < thk || idx < thi);
+    const unsigned msk = __ballot_sync(0xffffffffu, cand);
+    if (msk) *this = topk_offer_slow(*this, cand, msk, key, idx);
+}
 
 // ------------------------------------------------------------------ beta-slot run (reduce mode)
 // Evaluates `run` consecutive lane steps inside one alpha/beta block when n_beta = 32*M:
@@ -1268,7 +1286,7 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
                             t = dadd(t, dmul(pp_c, dadd(aval_pp, dmul(pp_s, brow[ts]))));
                         const double key = feas ? dmul(t, I) : CUDART_INF;
                         if (__any_sync(full, key <= tk.adm))
-                            tk.offer(feas, key, base + (uint64_t)(iL * C.nA + ia) * C.nB + ib);
+                            tk.offer_inl(feas, key, base + (uint64_t)(iL * C.nA + ia) * C.nB + ib);
                     }
                 }
         }
@@ -1512,7 +1530,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         lst[warp * PARADL_MAX_TOPK + lane].key_epoch_s = tk.ka;
         lst[warp * PARADL_MAX_TOPK + lane + 32].idx = tk.ib;
         lst[warp * PARADL_MAX_TOPK + lane + 32].key_epoch_s = tk.kb;
-        atomicAdd(&s_count, cnt);
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(full, cnt, o);
+        if (lane == 0) atomicAdd(&s_count, cnt);
         __syncthreads();
         bitonic_sort_smem(lst, kWarps * PARADL_MAX_TOPK);
         paradl_hit *out = a.cta_lists + (size_t)blockIdx.x * a.k;
