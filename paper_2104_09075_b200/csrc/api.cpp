@@ -656,7 +656,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD;
         const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
         const uint64_t Q = nAB * h.radix[D_LS] * h.radix[D_DIMS] * h.radix[D_S];
-        const uint64_t memo_n = (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]);
+        // memo: [n_b][n_S + n_dims] doubles; pd adds the ring GE table by (s, dims):
+        // [n_s][n_dims + 1] doubles (ge_c) + as many int32 (tier), n_s = max stage count + 1
+        const uint64_t n_stage = (h.part_mode == PARADL_PART_COMB ? (uint64_t)h.s_max : (uint64_t)h.G) + 1;
+        const uint64_t ctab_n = fam == PARADL_PD ? n_stage * (h.radix[D_DIMS] + 1) : 0;
+        const uint64_t memo_n = (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]) + ctab_n + (ctab_n + 1) / 2;
         const bool mask2 = h.part_mode == PARADL_PART_MASK && h.G >= 10 && h.radix[D_B] <= 2;
         const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22))
                              ? (mask2 ? 2 : 1)
@@ -694,6 +698,12 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 w.memo_n = (uint32_t)memo_n;
                 w.memo_off = a.memo_bytes;
                 a.memo_bytes += (uint32_t)align16(memo_n * sizeof(double));
+                if (mode == 1 && (fam == PARADL_PIPELINE || fam == PARADL_PD)) {
+                    // screened path: per-lane dims table (ge_c, ge_s fp64 + ge_t u8) per thread
+                    const uint32_t nD = h.radix[D_DIMS];
+                    const uint32_t tb = (uint32_t)align16((size_t)nD * 8u * kThreads);
+                    if (tb <= kMaxDtabBytes) a.dtab_bytes = std::max(a.dtab_bytes, tb);
+                }
                 if (mode == 2) {
                     w.low_off = a.low_bytes / 64;
                     a.low_bytes += h.radix[D_B] * 256u * 64u;
@@ -722,13 +732,14 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 by_mode[w.mode].work[by_mode[w.mode].n_work++] = w;
             }
             bool first = true;
-            const uint32_t memo_bytes = L[li].memo_bytes, low_bytes = L[li].low_bytes;
+            const uint32_t memo_bytes = L[li].memo_bytes, low_bytes = L[li].low_bytes, dtab_bytes = L[li].dtab_bytes;
             for (int md = 0; md < 3; md++) {
                 LaunchArgs &x = by_mode[md];
                 if (x.n_work == 0) continue;
                 if (md) {
                     x.memo_bytes = memo_bytes;
                     x.low_bytes = low_bytes;
+                    x.dtab_bytes = md == 1 ? dtab_bytes : 0;
                 }
                 if (first) {
                     L[li] = x;
@@ -760,7 +771,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     size_t total_ctas = 0;
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
-        smems[li] = smem + a.memo_bytes + a.low_bytes;
+        if (smem + a.memo_bytes + a.low_bytes + a.dtab_bytes > c->smem_optin) a.dtab_bytes = 0;   // unscreened path
+        smems[li] = smem + a.memo_bytes + a.low_bytes + a.dtab_bytes;
         const uint64_t okey = ((uint64_t)fam_of[li] << 40) | ((uint64_t)dense << 39) | ((uint64_t)blk_of[li] << 36) |
                               (uint64_t)smems[li];
         int nb = -1;

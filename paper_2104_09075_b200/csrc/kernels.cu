@@ -250,9 +250,10 @@ __device__ void stage_terms(const View &v, const Lane &L, const uint16_t *cuts, 
     const int G = M->G;
     st.maxF = st.maxB = st.maxU = st.maxW = st.maxY = st.sumY = st.memI = 0;
     const int64_t twob = 2 * b;
-    int beg = 0;
     uint64_t mask = L.part;
     const bool is_mask = v.S->part_mode == PARADL_PART_MASK;
+    // prefix values at the stage start, carried from the previous stage end
+    int64_t bF = PF[0], bB = PB[0], bU = PU[0], bW = PW[0], bX = PX[0], bI = PI[0];
     for (int i = 0; i < L.ns; i++) {
         int end;
         if (i == L.ns - 1) {
@@ -263,8 +264,10 @@ __device__ void stage_terms(const View &v, const Lane &L, const uint16_t *cuts, 
         } else {
             end = cuts[i * cs];
         }
-        int64_t F = PF[end] - PF[beg], B = PB[end] - PB[beg], U = PU[end] - PU[beg];
-        int64_t Wt = PW[end] - PW[beg], XY = PX[end] - PX[beg], BI = PI[end] - PI[beg];
+        const int64_t eF = PF[end], eB = PB[end], eU = PU[end], eW = PW[end], eX = PX[end], eI = PI[end];
+        int64_t F = eF - bF, B = eB - bB, U = eU - bU;
+        int64_t Wt = eW - bW, XY = eX - bX, BI = eI - bI;
+        bF = eF, bB = eB, bU = eU, bW = eW, bX = eX, bI = eI;
         st.maxF = F > st.maxF ? F : st.maxF;
         st.maxB = B > st.maxB ? B : st.maxB;
         st.maxU = U > st.maxU ? U : st.maxU;
@@ -276,7 +279,6 @@ __device__ void stage_terms(const View &v, const Lane &L, const uint16_t *cuts, 
             st.maxY = y > st.maxY ? y : st.maxY;
             st.sumY += y;
         }
-        beg = end;
     }
 }
 
@@ -1195,7 +1197,7 @@ __device__ __forceinline__ BlkCtx make_blk(const WorkItem &w, uint8_t *smem, con
 
 // Evaluates one partition (stage terms st, ns stages) and its inner block for the lane;
 // gblk = global index of the block's first configuration.  Whole warp (act per lane).
-template <int FAM>
+template <int FAM, bool COUNT = true>
 __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &L, const StageT &st, int64_t ns,
                                                uint64_t gblk, WarpTopK &tk, unsigned long long &cnt) {
     const View &v = C.v;
@@ -1269,7 +1271,7 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
                 }
             }
             const bool feas = act && r == 0;
-            cnt += feas ? C.nLAB : 0u;
+            if (COUNT) cnt += feas ? C.nLAB : 0u;
             if (__ballot_sync(full, feas) == 0u) continue;
             const uint64_t base = gblk + (uint64_t)(iS * C.nD + iD) * C.nLAB;
             for (uint32_t iL = 0; iL < C.nL; iL++)
@@ -1293,11 +1295,142 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
     }
 }
 
+// Screened evaluation of one partition's inner block (pipeline / pd, mode 1).  The keys
+// are the trees of eval_partition, with every term hoisted to the loop level it depends
+// on: per S value comp, pp_c, pp_s (4 S values per pass, in registers); per (alpha, beta)
+// row the pipeline term P = pp_c (alpha + pp_s beta); per dims value (innermost, from the
+// lane's smem table built once per partition) the GE term G = ge_c (alpha + ge_s beta).
+// Per configuration t = comp + G, t = t + P, key = t * I remain.  No top-k work is done
+// here: the block's smallest high word of the key bits is compared with the admission
+// bound once (for non-negative doubles key <= adm implies hi(key) <= hi(adm), so the
+// screen never drops a candidate), and a partition that passes is re-evaluated by
+// eval_partition, which offers its configurations one by one.  Infeasible terms are set
+// to +inf (key +inf, never below a finite bound); the feasible count is separable:
+// (#S with 1 <= S <= b) x (#dims in a tier) x n_LAB.
+// dtab: per-lane table [nD][kThreads] of ge_s; ge_c and ge_t come from the per-CTA ring
+// table by (stage count, dims value) built with the memo (pd, ring only: tree_thr = 0).
+// x / 2^k is exact (no underflow for x = 0 or x >= 1), so for power-of-two p_d the
+// division equals the multiplication by 2^-k bit for bit.
+__device__ __forceinline__ double div_by_count(double x, int64_t p) {
+    if (p > 0 && (p & (p - 1)) == 0 && p < (int64_t(1) << 62))
+        return dmul(x, __longlong_as_double((long long)(1023 - (63 - __clzll(p))) << 52));
+    return ddiv(x, i2d(p));
+}
+constexpr int kSB = 4;   // S values per pass
+template <int FAM>
+__device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, const Lane &L, const StageT &st,
+                                                        int64_t ns, uint64_t gblk, WarpTopK &tk,
+                                                        unsigned long long &cnt, double *dtab) {
+    const View &v = C.v;
+    const SubHdr *S = v.S;
+    const ImgHdr *H = v.H;
+    const unsigned full = 0xffffffffu;
+    const int NT = H->n_tiers;
+    const int64_t delta = H->delta;
+    const double INF = CUDART_INF;
+    double *gs_tab = dtab + threadIdx.x;
+    const uint32_t nDp = C.nD + 1;
+    const double *gc_row = C.memo + (size_t)S->radix[D_B] * (C.nS + C.nD);
+    const int32_t *gt_row = reinterpret_cast<const int32_t *>(
+        gc_row + (size_t)((S->part_mode == PARADL_PART_COMB ? S->s_max : S->G) + 1) * nDp);
+    int64_t b = 1;
+    double FBs = 0.0, Utau = 0.0, dmaxY = 0.0, part_inf = INF;
+    int ts = 0;
+    const double *mrow = C.memo;
+    uint32_t nSok = 0, nDok = 0;
+    if (act) {
+        b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
+        const double cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
+        const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
+        if (R != C.R_memo) {
+            C.R_memo = R;
+            C.tau = ddiv(1.0, R);
+        }
+        const int tsr = tier_of(H, ns);
+        ts = max(tsr, 0);
+        const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
+        part_inf = (tsr >= 0 && memv <= cap) ? 0.0 : INF;
+        FBs = i2d(st.maxF + st.maxB);
+        Utau = dmul(i2d(st.maxU), C.tau);
+        dmaxY = i2d(delta * st.maxY);
+        mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
+        if (FAM == PARADL_PD) {
+            const double mW = i2d(delta * st.maxW);
+            gc_row += (size_t)ns * nDp;
+            gt_row += (size_t)ns * nDp;
+            for (uint32_t iD = 0; iD < C.nD; iD++) {
+                nDok += gc_row[iD] != INF ? 1u : 0u;
+                gs_tab[(size_t)iD * kThreads] = div_by_count(mW, C.dmv[4 * iD]);
+            }
+        } else {
+            nDok = C.nD;
+        }
+    }
+    const double tau = C.tau;
+    int hmin = 0x7fffffff;
+    for (uint32_t iS0 = 0; iS0 < C.nS; iS0 += kSB) {
+        double comp[kSB], ppc[kSB], pps[kSB];
+#pragma unroll
+        for (int u = 0; u < kSB; u++) {
+            comp[u] = INF;
+            ppc[u] = pps[u] = 0.0;
+            const uint32_t iS = iS0 + u;
+            if (act && iS < C.nS) {
+                const int64_t Sg = C.Sv[iS];
+                const double bS = mrow[iS];
+                const double cseg = dmul(i2d(ns + Sg - 1), bS);
+                const bool sok = Sg >= 1 && Sg <= b;
+                nSok += sok ? 1u : 0u;
+                comp[u] = dadd(dadd(dmul(dmul(cseg, FBs), tau), Utau), sok ? part_inf : INF);
+                if (ns > 1) {
+                    ppc[u] = i2d(2 * (ns + Sg - 2));
+                    pps[u] = dmul(bS, dmaxY);
+                }
+            }
+        }
+        for (uint32_t iL = 0; iL < C.nL; iL++)
+            for (uint32_t ia = 0; ia < C.nA; ia++) {
+                const double *arow = C.alpha_tab + (size_t)ia * NT;
+                const double at_ = arow[ts];
+                for (uint32_t ib = 0; ib < C.nB; ib++) {
+                    const double *brow = C.beta_tab + (size_t)ib * NT;
+                    const double bt_ = brow[ts];
+                    double P[kSB];
+#pragma unroll
+                    for (int u = 0; u < kSB; u++) P[u] = dmul(ppc[u], dadd(at_, dmul(pps[u], bt_)));
+                    if (FAM == PARADL_PD) {
+#pragma unroll 2
+                        for (uint32_t iD = 0; iD < C.nD; iD++) {
+                            const double I = mrow[C.nS + iD];
+                            const int gt = gt_row[iD];
+                            const double G =
+                                dmul(gc_row[iD], dadd(arow[gt], dmul(gs_tab[(size_t)iD * kThreads], brow[gt])));
+#pragma unroll
+                            for (int u = 0; u < kSB; u++)
+                                hmin = min(hmin, __double2hiint(dmul(dadd(dadd(comp[u], G), P[u]), I)));
+                        }
+                    } else {
+                        for (uint32_t iD = 0; iD < C.nD; iD++) {
+                            const double I = mrow[C.nS + iD];
+#pragma unroll
+                            for (int u = 0; u < kSB; u++)
+                                hmin = min(hmin, __double2hiint(dmul(dadd(comp[u], P[u]), I)));
+                        }
+                    }
+                }
+            }
+    }
+    if (act && part_inf == 0.0) cnt += (unsigned long long)nSok * nDok * C.nLAB;
+    const bool maybe = act && hmin <= __double2hiint(tk.adm);
+    if (__any_sync(full, maybe)) eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
+}
+
 // Mode 1: lane l of tile t owns partitions [t*32c + l*c, +c) of the block-aligned range;
 // stage terms by prefix differences, successor between partitions.
 template <int FAM>
 __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
-                                  uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo) {
+                                  uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
+                                  double *dtab) {
     BlkCtx C = make_blk(w, smem, memo);
     const int lane = threadIdx.x & 31;
     const uint64_t nblk = (w.hi - w.lo) / C.Q;
@@ -1315,7 +1448,12 @@ __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64
             stage_terms(C.v, L, cuts, kThreads, at<int64_t>(C.v.img, C.v.S->off_b)[L.d[D_B]], st);
             ns = L.ns;
         }
-        eval_partition<FAM>(C, act, L, st, ns, C.v.S->offset + w.lo + (blk0 + it) * C.Q, tk, cnt);
+        const uint64_t gblk = C.v.S->offset + w.lo + (blk0 + it) * C.Q;
+        if ((FAM == PARADL_PIPELINE || (FAM == PARADL_PD && C.v.H->tree_thr <= 0.0)) && dtab &&
+            (size_t)C.nD * 8u * kThreads <= a.dtab_bytes)
+            eval_partition_screened<FAM>(C, act, L, st, ns, gblk, tk, cnt, dtab);
+        else
+            eval_partition<FAM>(C, act, L, st, ns, gblk, tk, cnt);
         tk.refresh();
         if (it + 1 < nmine) advance(w, C.v, L, cuts, kThreads);   // next partition (inc_part = 1)
     }
@@ -1439,7 +1577,23 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
         const int64_t *bv = at<int64_t>(v.img, S->off_b);
         const int32_t *Sv = at<int32_t>(v.img, S->off_S);
         const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
-        for (uint32_t e = threadIdx.x; e < w.memo_n; e += blockDim.x) {
+        const uint32_t nrow = S->radix[D_B] * (nS + nD);
+        if (w.family == PARADL_PD && w.mode == 1) {
+            // ring GE coefficient and tier per (stage count s, dims value): make_ar's ring
+            // branch, ge_c = 2 (p_d - 1) (0 when p_d = 1), +inf when s p_d exceeds every tier
+            const uint32_t nDp = nD + 1;
+            const uint32_t n_stage = (S->part_mode == PARADL_PART_COMB ? S->s_max : S->G) + 1;
+            double *gc = tab + nrow;
+            int32_t *gt = reinterpret_cast<int32_t *>(gc + n_stage * nDp);
+            for (uint32_t e = threadIdx.x; e < n_stage * nDp; e += blockDim.x) {
+                const uint32_t sv = e / nDp, iD = e - sv * nDp;
+                const int64_t pd = iD < nD ? dmv[4 * iD] : 1;
+                const int tp = tier_of(v.H, (int64_t)sv * pd);
+                gc[e] = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
+                gt[e] = max(tp, 0);
+            }
+        }
+        for (uint32_t e = threadIdx.x; e < nrow; e += blockDim.x) {
             const uint32_t ib = e / (nS + nD), j = e - ib * (nS + nD);
             const int64_t b = bv[ib];
             if (j < nS) tab[e] = ddiv(i2d(b), i2d(Sv[j]));
@@ -1503,6 +1657,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
     double *memo = reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra));
     LowE *lowtab = reinterpret_cast<LowE *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes);
+    double *dtab = a.dtab_bytes ? reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes +
+                                                             a.low_bytes)
+                                : nullptr;
     if (BLK) build_memo(a, smem, memo, lowtab);
 
     for (;;) {
@@ -1515,7 +1672,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         while (wi + 1 < a.n_work && T >= a.work[wi + 1].tile_base) wi++;
         const WorkItem &w = a.work[wi];
         if (BLK == 1)
-            tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo);
+            tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, dtab);
         else if (BLK == 2)
             tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
         else

@@ -22,6 +22,7 @@ constexpr int kMaxWork = 8;              // work items per sweep launch (kernel 
 constexpr int kMaxModelsPerSweep = 8;
 constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 
 // digits of the canonical mixed radix, fast -> slow
@@ -105,7 +106,8 @@ struct LaunchArgs {
     uint64_t total_tiles;
     int32_t shard, n_shards;
     unsigned long long *tile_counter;
-    int32_t k, pad;
+    int32_t k;
+    uint32_t dtab_bytes;           // mode-1 screened path: per-lane dims tables after the low tables
     paradl_hit *cta_lists;         // [gridDim.x][k] (reduce mode)
     unsigned long long *count;     // feasible count accumulator (reduce mode)
     unsigned long long *gbound;    // shared top-k admission bound (reduce mode; ~0 = none)

@@ -289,6 +289,37 @@ def test_lane_blocked_modes(dev, oracle_mod, seed, G, fam):
         check_topk(ctx, spec, osw, a, c, rng.choice([3, 33]))
 
 
+@pytest.mark.parametrize("seed,fam,tree", [(21, W.PD, 0.0), (22, W.PD, 1e6), (23, W.PIPELINE, 0.0),
+                                           (24, W.PD, 0.0)])
+def test_lane_blocked_screened(dev, oracle_mod, seed, fam, tree):
+    """Mode-1 screened path (pipeline / pd, ring collectives): several S passes (7 S values,
+    one ragged pass), S > b (Segments), power-of-two and other p_d (exact-division shortcut vs
+    IEEE division), p_d beyond every tier (Tier), memory-infeasible stages; tree_threshold > 0
+    takes the unscreened path.  Whole sweep and ragged windows against the oracle."""
+    import dataclasses
+    m = corpus.random_model(seed, G=12)
+    sysd = dataclasses.replace(corpus.random_system(seed), tree_threshold=tree)
+    nt = len(sysd.tiers)
+    A = [[1e-6 * (i + 1) * (t + 1) for t in range(nt)] for i in range(2)]
+    Bt = [[1e-10 * (i + 3) * (t + 1) for t in range(nt)] for i in range(2)]
+    common = dict(b=[3, 16], S=[1, 2, 3, 4, 5, 8, 32], alpha=A, beta=Bt, cap=[2.0 ** 22, 2.0 ** 40])
+    if fam == W.PD:
+        common["dims"] = [(p, 1, 1, 1) for p in (1, 2, 3, 6, 8, 48, 1024, 4096)]
+    subs = [W.SubSweep(fam, part_mode=W.PART_COMB, s_min=1, s_max=5, **common)]
+    sw = W.Sweep([m], sysd, subs, "screened")
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    for k in (1, 64):
+        check_topk(ctx, spec, osw, 0, n, k)
+    rng = random.Random(seed)
+    for _ in range(3):
+        a = rng.randrange(n)
+        c = rng.randrange(1, n - a + 1)
+        check_topk(ctx, spec, osw, a, c, rng.choice([5, 64]))
+
+
 def test_unaligned_windows_all_families(dev, oracle_mod):
     """Ranges starting at every residue mod 32 (lane/slot alignment edge cases), cfg2 shapes."""
     sw = W.config2(n_alpha=3, n_beta=64, b_list=[2, 64], pipe_smax=2)
