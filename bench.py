@@ -38,6 +38,22 @@ FP64_OPS_PER_CONFIG = {"pipeline": 5, "data": 5, "filter": 7, "channel": 7, "spa
                        "ds": 11, "pd": 8, "layerpure": 5, "serial": 3}
 
 
+def fp64_per_config(sb) -> float:
+    """Algorithmic FP64 instructions per feasible configuration of a sub-sweep.
+    Pipeline / pd sub-sweeps with a small alpha x beta block run the lane-blocked screened
+    nest: per configuration t = comp + G, t += P, key = t * I (pd; pipeline has no G), with
+    G = ge_c (alpha + ge_s beta) shared by the 4 S values of a pass and P = pp_c (alpha +
+    pp_s beta) shared by the dims values; the admission screen is an integer min."""
+    from workloads import sweeps as W
+    fam = W.FAMILY_NAMES[sb.family]
+    nab = max(1, len(sb.alpha)) * max(1, len(sb.beta))
+    if fam in ("pd", "pipeline") and nab < 32:
+        n_s, n_d = max(1, len(sb.S)), max(1, len(sb.dims))
+        g = 3.0 * math.ceil(n_s / 4) / n_s if fam == "pd" else 0.0
+        return (3.0 if fam == "pd" else 2.0) + g + 3.0 / n_d
+    return float(FP64_OPS_PER_CONFIG[fam])
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -317,7 +333,8 @@ def ours(args):
         n_feas = int(my_cnt.item())
         # algorithmic FP64 work: the cost tree runs for feasible configurations only (the
         # others are rejected by integer / single-compare checks before any FP64 work)
-        ops = n_feas * FP64_OPS_PER_CONFIG[fam_name]
+        opc = fp64_per_config(sweep.subs[di])
+        ops = n_feas * opc
         achieved = ops / (kms * 1e-3) / 1e12
         peak = fp64_peak / 1e12
         traffic = None
@@ -330,7 +347,7 @@ def ours(args):
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T fp64-pipe inst/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": f"sweep_kernel<{fam_name.upper()},reduce> (+merge)", "configs_per_launch": nd,
-                "fp64_inst_per_config": FP64_OPS_PER_CONFIG[fam_name], "feasible_configs": n_feas,
+                "fp64_inst_per_config": opc, "feasible_configs": n_feas,
                 "launch_ms": kms,
                 "peak_source": "measured DFMA-chain microbenchmark (paradl_fp64_peak) in this run",
                 "peak_nominal_T": 148 * 64 * 1.965e9 / 1e12,

@@ -237,8 +237,48 @@ struct StageT {
 
 // Per-stage sums FW_{G_i} = sum_{l in g_i} FW_l by prefix differences; maxima
 // as in Table 2's Layer row.  b = per-replica batch (memory, Q6).
+// stage_span folds stages i0..i1-1 (stage i ends at cut i, the last one at G; COMB cuts) that
+// start at row beg into st; all terms are exact int64 maxima / sums, so any split of the
+// stage list composes to the same StageT.
+__device__ __forceinline__ void stage_span(const View &v, const uint16_t *cuts, int cs, int64_t twob, int ns,
+                                           int i0, int i1, int beg, StageT &st) {
+    const ModelHdr *M = v.M;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+    const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+    const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    // prefix values at the stage start, carried from the previous stage end
+    int64_t bF = PF[beg], bB = PB[beg], bU = PU[beg], bW = PW[beg], bX = PX[beg], bI = PI[beg];
+    for (int i = i0; i < i1; i++) {
+        const int end = i == ns - 1 ? M->G : cuts[i * cs];
+        const int64_t eF = PF[end], eB = PB[end], eU = PU[end], eW = PW[end], eX = PX[end], eI = PI[end];
+        const int64_t F = eF - bF, B = eB - bB, U = eU - bU;
+        const int64_t Wt = eW - bW, XY = eX - bX, BI = eI - bI;
+        bF = eF, bB = eB, bU = eU, bW = eW, bX = eX, bI = eI;
+        st.maxF = F > st.maxF ? F : st.maxF;
+        st.maxB = B > st.maxB ? B : st.maxB;
+        st.maxU = U > st.maxU ? U : st.maxU;
+        st.maxW = Wt > st.maxW ? Wt : st.maxW;
+        const int64_t mem = twob * XY + 2 * Wt + BI;
+        st.memI = mem > st.memI ? mem : st.memI;
+        if (i < ns - 1) {
+            const int64_t y = Y[end - 1];
+            st.maxY = y > st.maxY ? y : st.maxY;
+            st.sumY += y;
+        }
+    }
+}
+
 __device__ void stage_terms(const View &v, const Lane &L, const uint16_t *cuts, int cs, int64_t b,
                             StageT &st) {
+    st.maxF = st.maxB = st.maxU = st.maxW = st.maxY = st.sumY = st.memI = 0;
+    if (v.S->part_mode != PARADL_PART_MASK) {
+        stage_span(v, cuts, cs, 2 * b, L.ns, 0, L.ns, 0, st);
+        return;
+    }
     const ModelHdr *M = v.M;
     const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
     const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
@@ -248,34 +288,29 @@ __device__ void stage_terms(const View &v, const Lane &L, const uint16_t *cuts, 
     const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
     const int64_t *Y = at<int64_t>(v.mb, M->off_y);
     const int G = M->G;
-    st.maxF = st.maxB = st.maxU = st.maxW = st.maxY = st.sumY = st.memI = 0;
     const int64_t twob = 2 * b;
     uint64_t mask = L.part;
-    const bool is_mask = v.S->part_mode == PARADL_PART_MASK;
-    // prefix values at the stage start, carried from the previous stage end
     int64_t bF = PF[0], bB = PB[0], bU = PU[0], bW = PW[0], bX = PX[0], bI = PI[0];
     for (int i = 0; i < L.ns; i++) {
         int end;
         if (i == L.ns - 1) {
             end = G;
-        } else if (is_mask) {
+        } else {
             end = __ffsll((long long)mask);   // bit j set <=> cut after row j+1
             mask &= mask - 1;
-        } else {
-            end = cuts[i * cs];
         }
         const int64_t eF = PF[end], eB = PB[end], eU = PU[end], eW = PW[end], eX = PX[end], eI = PI[end];
-        int64_t F = eF - bF, B = eB - bB, U = eU - bU;
-        int64_t Wt = eW - bW, XY = eX - bX, BI = eI - bI;
+        const int64_t F = eF - bF, B = eB - bB, U = eU - bU;
+        const int64_t Wt = eW - bW, XY = eX - bX, BI = eI - bI;
         bF = eF, bB = eB, bU = eU, bW = eW, bX = eX, bI = eI;
         st.maxF = F > st.maxF ? F : st.maxF;
         st.maxB = B > st.maxB ? B : st.maxB;
         st.maxU = U > st.maxU ? U : st.maxU;
         st.maxW = Wt > st.maxW ? Wt : st.maxW;
-        int64_t mem = twob * XY + 2 * Wt + BI;
+        const int64_t mem = twob * XY + 2 * Wt + BI;
         st.memI = mem > st.memI ? mem : st.memI;
         if (i < L.ns - 1) {
-            int64_t y = Y[end - 1];
+            const int64_t y = Y[end - 1];
             st.maxY = y > st.maxY ? y : st.maxY;
             st.sumY += y;
         }
@@ -1172,6 +1207,7 @@ struct BlkCtx {
     uint32_t nB, nA, nL, nD, nS, nLAB;
     uint64_t Q;
     double R_memo, tau;
+    double mW_tab;   // screened pd: mW the lane's ge_s table holds (NaN: none)
 };
 
 __device__ __forceinline__ BlkCtx make_blk(const WorkItem &w, uint8_t *smem, const double *memo) {
@@ -1192,6 +1228,7 @@ __device__ __forceinline__ BlkCtx make_blk(const WorkItem &w, uint8_t *smem, con
     C.Q = (uint64_t)C.nS * C.nD * C.nLAB;
     C.R_memo = -1.0;
     C.tau = 0.0;
+    C.mW_tab = CUDART_NAN;
     return C;
 }
 
@@ -1309,13 +1346,8 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
 // (#S with 1 <= S <= b) x (#dims in a tier) x n_LAB.
 // dtab: per-lane table [nD][kThreads] of ge_s; ge_c and ge_t come from the per-CTA ring
 // table by (stage count, dims value) built with the memo (pd, ring only: tree_thr = 0).
-// x / 2^k is exact (no underflow for x = 0 or x >= 1), so for power-of-two p_d the
-// division equals the multiplication by 2^-k bit for bit.
-__device__ __forceinline__ double div_by_count(double x, int64_t p) {
-    if (p > 0 && (p & (p - 1)) == 0 && p < (int64_t(1) << 62))
-        return dmul(x, __longlong_as_double((long long)(1023 - (63 - __clzll(p))) << 52));
-    return ddiv(x, i2d(p));
-}
+// ge_s = mW / p_d: x / 2^k is exact (x = 0 or x >= 1: no underflow), so for power-of-two
+// p_d the division equals the multiplication by the scale 2^-k (ring table row 0) bit for bit.
 constexpr int kSB = 4;   // S values per pass
 template <int FAM>
 __device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, const Lane &L, const StageT &st,
@@ -1356,12 +1388,16 @@ __device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, con
         mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
         if (FAM == PARADL_PD) {
             const double mW = i2d(delta * st.maxW);
+            if (mW != C.mW_tab) {   // ge_s = mW / p_d (the lane's table is kept while mW repeats)
+                C.mW_tab = mW;
+                for (uint32_t iD = 0; iD < C.nD; iD++) {
+                    const double sc = gc_row[iD];
+                    gs_tab[(size_t)iD * kThreads] = sc != 0.0 ? dmul(mW, sc) : ddiv(mW, i2d(C.dmv[4 * iD]));
+                }
+            }
             gc_row += (size_t)ns * nDp;
             gt_row += (size_t)ns * nDp;
-            for (uint32_t iD = 0; iD < C.nD; iD++) {
-                nDok += gc_row[iD] != INF ? 1u : 0u;
-                gs_tab[(size_t)iD * kThreads] = div_by_count(mW, C.dmv[4 * iD]);
-            }
+            nDok = (uint32_t)gt_row[C.nD];
         } else {
             nDok = C.nD;
         }
@@ -1427,6 +1463,10 @@ __device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, con
 
 // Mode 1: lane l of tile t owns partitions [t*32c + l*c, +c) of the block-aligned range;
 // stage terms by prefix differences, successor between partitions.
+#ifndef PARADL_INC_STAGES
+#define PARADL_INC_STAGES 0
+#endif
+constexpr bool kIncStages = PARADL_INC_STAGES;
 template <int FAM>
 __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
                                   uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
@@ -1439,13 +1479,32 @@ __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64
     const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
     const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
     Lane L;
-    StageT st;
+    StageT st, pre;
+    // COMB successors mostly move only the last cut: stages 0..ns-3 (ending at cut ns-3)
+    // are then unchanged, so their folded terms `pre` are reused and only the last two
+    // stages are recomputed (pre_key: ns, b digit and cut ns-3 it was built for)
+    const bool comb = kIncStages && C.v.S->part_mode == PARADL_PART_COMB;
+    uint64_t pre_key = ~0ull;
     if (nmine) decode(C.v, w.lo + blk0 * C.Q, L, cuts, kThreads);
     for (uint32_t it = 0; it < iters; it++) {
         const bool act = it < nmine;
         int64_t ns = 1;
         if (act) {
-            stage_terms(C.v, L, cuts, kThreads, at<int64_t>(C.v.img, C.v.S->off_b)[L.d[D_B]], st);
+            const int64_t b = at<int64_t>(C.v.img, C.v.S->off_b)[L.d[D_B]];
+            if (comb) {
+                const int k2 = L.ns - 3;   // last stage of the reusable prefix
+                const int c2 = k2 >= 0 ? cuts[k2 * kThreads] : 0;
+                const uint64_t key = ((uint64_t)L.ns << 48) | ((uint64_t)L.d[D_B] << 16) | (uint64_t)c2;
+                if (key != pre_key) {
+                    pre_key = key;
+                    pre.maxF = pre.maxB = pre.maxU = pre.maxW = pre.maxY = pre.sumY = pre.memI = 0;
+                    if (k2 >= 0) stage_span(C.v, cuts, kThreads, 2 * b, L.ns, 0, k2 + 1, 0, pre);
+                }
+                st = pre;
+                stage_span(C.v, cuts, kThreads, 2 * b, L.ns, max(k2 + 1, 0), L.ns, c2, st);
+            } else {
+                stage_terms(C.v, L, cuts, kThreads, b, st);
+            }
             ns = L.ns;
         }
         const uint64_t gblk = C.v.S->offset + w.lo + (blk0 + it) * C.Q;
@@ -1585,12 +1644,26 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
             const uint32_t n_stage = (S->part_mode == PARADL_PART_COMB ? S->s_max : S->G) + 1;
             double *gc = tab + nrow;
             int32_t *gt = reinterpret_cast<int32_t *>(gc + n_stage * nDp);
+            // row s = 0 (no such stage count) holds the exact scale 2^-k of power-of-two p_d
+            // (0: divide); column n_dims of gt holds the number of dims values in a tier
             for (uint32_t e = threadIdx.x; e < n_stage * nDp; e += blockDim.x) {
                 const uint32_t sv = e / nDp, iD = e - sv * nDp;
                 const int64_t pd = iD < nD ? dmv[4 * iD] : 1;
-                const int tp = tier_of(v.H, (int64_t)sv * pd);
-                gc[e] = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
-                gt[e] = max(tp, 0);
+                if (sv == 0) {
+                    gc[e] = (pd > 0 && (pd & (pd - 1)) == 0)
+                                ? __longlong_as_double((long long)(1023 - (63 - __clzll(pd))) << 52)
+                                : 0.0;
+                    gt[e] = 0;
+                } else if (iD == nD) {
+                    int ok = 0;
+                    for (uint32_t j = 0; j < nD; j++) ok += tier_of(v.H, (int64_t)sv * dmv[4 * j]) >= 0;
+                    gc[e] = 0.0;
+                    gt[e] = ok;
+                } else {
+                    const int tp = tier_of(v.H, (int64_t)sv * pd);
+                    gc[e] = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
+                    gt[e] = max(tp, 0);
+                }
             }
         }
         for (uint32_t e = threadIdx.x; e < nrow; e += blockDim.x) {
