@@ -1532,6 +1532,24 @@ struct LowE {
 };
 static_assert(sizeof(LowE) == 64, "LowE layout");
 
+// Largest integer m with gamma (delta m) <= cap (Table 2 mem row), -1 if none:
+// i2d and multiplication by a positive constant are monotone, so the predicate is a
+// down-set in m and the integer compare m <= threshold decides exactly what the fp64
+// compare decides (memI < 2^62 by the host's overflow bounds).
+__device__ __noinline__ int64_t mem_threshold(const ImgHdr *H, double cap) {
+    const double g = H->gamma, d = i2d(H->delta);
+    auto ok = [&](int64_t m) { return dmul(g, dmul(d, i2d(m))) <= cap; };
+    if (!ok(0)) return -1;
+    int64_t lo = 0, hi = int64_t(1) << 62;
+    if (ok(hi)) return hi;
+    while (hi - lo > 1) {   // ok(lo), !ok(hi)
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (ok(mid)) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 template <int FAM>
 __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
                                uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
@@ -1556,6 +1574,9 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
     Lane L;
     if (nmine) decode(v, w.lo + blk0 * span, L, cuts, kThreads);
+    const bool screen = FAM == PARADL_PIPELINE && C.Q == 1;
+    double cap_memo = CUDART_NAN;
+    int64_t mem_max = -1;
     for (uint32_t it = 0; it < iters; it++) {
         const bool act = it < nmine;
         // high part of this block: stages after the first high cut
@@ -1599,24 +1620,81 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
             }
         }
         const uint64_t gbase = v.S->offset + w.lo + (blk0 + it) * span;
-        for (uint32_t x = 0; x < (1u << kLowBits); x++) {
-            StageT st;
-            int64_t ns = 1;
+        bool maybe = act;
+        if (screen) {
+            // screened block (pipeline, one configuration per mask): every key with the trees
+            // of eval_partition, only the smallest high word kept; memory feasibility by the
+            // integer threshold memI <= mem_max (gamma (delta memI) is monotone in memI)
+            int hmin = 0x7fffffff;
             if (act) {
-                const LowE e = lt[x];
-                const int beg = e.e_last;
-                const int64_t F = PF[c_h] - PF[beg], Bw = PB[c_h] - PB[beg], U = PU[c_h] - PU[beg];
-                const int64_t Wt = PW[c_h] - PW[beg], XY = PX[c_h] - PX[beg], BI = PI[c_h] - PI[beg];
-                st.maxF = max(max(e.F, F), hF);
-                st.maxB = max(max(e.B, Bw), hB);
-                st.maxU = max(max(e.U, U), hU);
-                st.maxW = max(max(e.W, Wt), hW);
-                st.memI = max(max(e.memI, 2 * b * XY + 2 * Wt + BI), hM);
-                st.maxY = max(e.maxY, hY);
-                st.sumY = e.sumY + hS;
-                ns = e.pop + hpop + 1;
+                const ImgHdr *H = v.H;
+                const double cap = at<double>(v.img, v.S->off_cap)[L.d[D_CAP]];
+                const double R = at<double>(v.img, v.S->off_flops)[L.d[D_FLOPS]];
+                if (R != C.R_memo) {
+                    C.R_memo = R;
+                    C.tau = ddiv(1.0, R);
+                }
+                if (!(cap == cap_memo)) {
+                    cap_memo = cap;
+                    mem_max = mem_threshold(H, cap);
+                }
+                const double tau = C.tau;
+                const double *mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
+                const double bS = mrow[0], I = mrow[C.nS];
+                const int64_t Sg = C.Sv[0];
+                const bool seg_ok = Sg >= 1 && Sg <= b;
+                const int64_t delta = H->delta;
+                const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
+                uint32_t nok = 0;
+#pragma unroll 2
+                for (uint32_t x = 0; x < (1u << kLowBits); x++) {
+                    const LowE e = lt[x];
+                    const int beg = e.e_last;
+                    const int64_t maxF = max(max(e.F, cF - PF[beg]), hF);
+                    const int64_t maxB = max(max(e.B, cB - PB[beg]), hB);
+                    const int64_t maxU = max(max(e.U, cU - PU[beg]), hU);
+                    const int64_t memI = max(max(e.memI, 2 * b * (cX - PX[beg]) + 2 * (cW - PW[beg]) + (cI - PI[beg])), hM);
+                    const int64_t maxY = max(e.maxY, hY);
+                    const int64_t ns = e.pop + hpop + 1;
+                    const int tsr = tier_of(H, ns);
+                    const int ts = max(tsr, 0);
+                    const bool feas = seg_ok && tsr >= 0 && memI <= mem_max;
+                    const double cseg = dmul(i2d(ns + Sg - 1), bS);
+                    const double comp = dadd(dmul(dmul(cseg, i2d(maxF + maxB)), tau), dmul(i2d(maxU), tau));
+                    const double ppc = ns > 1 ? i2d(2 * (ns + Sg - 2)) : 0.0;
+                    const double pps = ns > 1 ? dmul(bS, i2d(delta * maxY)) : 0.0;
+                    const double key =
+                        dmul(dadd(comp, dmul(ppc, dadd(C.alpha_tab[ts], dmul(pps, C.beta_tab[ts])))), I);
+                    nok += feas ? 1u : 0u;
+                    hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
+                }
+                cnt += nok;
             }
-            eval_partition<FAM>(C, act, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
+            maybe = act && hmin <= __double2hiint(tk.adm);
+        }
+        if (!screen || __any_sync(0xffffffffu, maybe)) {
+            for (uint32_t x = 0; x < (1u << kLowBits); x++) {
+                StageT st;
+                int64_t ns = 1;
+                if (maybe) {
+                    const LowE e = lt[x];
+                    const int beg = e.e_last;
+                    const int64_t F = PF[c_h] - PF[beg], Bw = PB[c_h] - PB[beg], U = PU[c_h] - PU[beg];
+                    const int64_t Wt = PW[c_h] - PW[beg], XY = PX[c_h] - PX[beg], BI = PI[c_h] - PI[beg];
+                    st.maxF = max(max(e.F, F), hF);
+                    st.maxB = max(max(e.B, Bw), hB);
+                    st.maxU = max(max(e.U, U), hU);
+                    st.maxW = max(max(e.W, Wt), hW);
+                    st.memI = max(max(e.memI, 2 * b * XY + 2 * Wt + BI), hM);
+                    st.maxY = max(e.maxY, hY);
+                    st.sumY = e.sumY + hS;
+                    ns = e.pop + hpop + 1;
+                }
+                if (screen)
+                    eval_partition<FAM, false>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
+                else
+                    eval_partition<FAM>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
+            }
         }
         tk.refresh();
         if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 256

@@ -320,6 +320,31 @@ def test_lane_blocked_screened(dev, oracle_mod, seed, fam, tree):
         check_topk(ctx, spec, osw, a, c, rng.choice([5, 64]))
 
 
+@pytest.mark.parametrize("seed,G,S", [(31, 12, 4), (32, 16, 1), (33, 14, 8), (34, 13, 2)])
+def test_mask_blocks_screened(dev, oracle_mod, seed, G, S):
+    """Mode-2 screened path (pipeline masks, one configuration per mask as in cfg3-ii):
+    memory threshold, tier of the stage count, S > b, two b values, ragged windows."""
+    m = corpus.random_model(seed, G=G)
+    sysd = corpus.random_system(seed)
+    nt = len(sysd.tiers)
+    A = [[2e-6 * (t + 1) for t in range(nt)]]
+    Bt = [[3e-10 * (t + 1) for t in range(nt)]]
+    subs = [W.SubSweep(W.PIPELINE, part_mode=W.PART_MASK, b=[4, 16], S=[S], alpha=A, beta=Bt,
+                       cap=[2.0 ** 18, 2.0 ** 24, 2.0 ** 40])]
+    sw = W.Sweep([m], sysd, subs, "mask_screened")
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    for k in (1, 64):
+        check_topk(ctx, spec, osw, 0, n, k)
+    rng = random.Random(seed)
+    for _ in range(3):
+        a = rng.randrange(n)
+        c = rng.randrange(1, n - a + 1)
+        check_topk(ctx, spec, osw, a, c, rng.choice([7, 64]))
+
+
 def test_unaligned_windows_all_families(dev, oracle_mod):
     """Ranges starting at every residue mod 32 (lane/slot alignment edge cases), cfg2 shapes."""
     sw = W.config2(n_alpha=3, n_beta=64, b_list=[2, 64], pipe_smax=2)
