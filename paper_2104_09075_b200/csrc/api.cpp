@@ -27,7 +27,7 @@ struct HostModel {
     ModelHdr layout{};
     uint8_t *d_block = nullptr;
     // host-side bounds for overflow proofs only
-    __int128 FB = 0, XY = 0, W = 0, BI = 0, Ysum = 0, Ymax = 0, Hmax = 0;
+    __int128 FB = 0, XY = 0, W = 0, BI = 0, Ysum = 0, Ymax = 0, Hmax = 0, WU = 0;
 };
 
 struct DevBuf {
@@ -203,6 +203,7 @@ extern "C" paradl_status paradl_load_model(paradl_ctx *c, const paradl_layer *ro
         if (st) return st;
         const paradl_layer &r = rows[l];
         m.FB += (__int128)r.fw + r.bw;
+        m.WU += r.wu;
         m.XY += (__int128)r.x + r.y;
         m.W += r.w;
         m.BI += r.bi;
@@ -281,6 +282,7 @@ namespace {
 struct SubPlan {
     SubHdr hdr{};
     int family = 0, model = 0;   // model = ctx model id
+    int64_t bmax = 0;            // largest batch value
 };
 
 struct Plan {
@@ -472,6 +474,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         h.off_sblk = put(sblk.data(), sblk.size() * 8);
         sp.family = fam;
         sp.model = s.model_id;
+        sp.bmax = bmax;
         P.subs.push_back(sp);
     }
     P.total = (uint64_t)total;
@@ -703,6 +706,16 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     const uint32_t nD = h.radix[D_DIMS];
                     const uint32_t tb = (uint32_t)align16((size_t)nD * 8u * kThreads);
                     if (tb <= kMaxDtabBytes) a.dtab_bytes = std::max(a.dtab_bytes, tb);
+                }
+                if (mode == 2 && fam == PARADL_PIPELINE && Q == 1) {
+                    // screened mask blocks hold every stage quantity as an exact double: the
+                    // model totals bound each stage term, so they must stay below 2^53
+                    const HostModel &hm = c->models[P.subs[q].model];
+                    const int64_t bmax = P.subs[q].bmax;
+                    const __int128 lim = (__int128)1 << 53;
+                    const __int128 memb = 2 * (__int128)bmax * hm.XY + 2 * hm.W + hm.BI;
+                    if (hm.FB < lim && hm.WU < lim && memb < lim && (__int128)c->sys.delta * hm.Ymax < lim)
+                        w.flags |= kWorkMaskD;
                 }
                 if (mode == 2) {
                     w.low_off = a.low_bytes / 64;

@@ -1001,6 +1001,7 @@ __device__ void bitonic_sort_smem(paradl_hit *x, int n) {
 struct SmemExtra {
     uint16_t cuts[kMaxCuts][kThreads];
     paradl_hit lists[kWarps][PARADL_MAX_TOPK];
+    int8_t tier_by_n[PARADL_MAX_STAGES + 8];   // tier_of(n), n <= 64 (mask stage counts)
 };
 
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
@@ -1531,6 +1532,13 @@ struct LowE {
     int32_t e_last, pop;
 };
 static_assert(sizeof(LowE) == 64, "LowE layout");
+// the same low-bit table as exact doubles (kWorkMaskD: every stage term < 2^53)
+struct LowD {
+    double F, B, U, M, Y;
+    int32_t pop, e_last;
+    double pad_[2];
+};
+static_assert(sizeof(LowD) == 64, "LowD layout");
 
 // Largest integer m with gamma (delta m) <= cap (Table 2 mem row), -1 if none:
 // i2d and multiplication by a positive constant are monotone, so the predicate is a
@@ -1548,6 +1556,147 @@ __device__ __noinline__ int64_t mem_threshold(const ImgHdr *H, double cap) {
         else hi = mid;
     }
     return lo;
+}
+
+// Mode 2, screened (pipeline, one configuration per mask: the cfg3-ii shape; kWorkMaskD).
+// Stage terms are exact doubles (host bound < 2^53), so maxima are DMNMX and no int64 ->
+// fp64 conversion is left per mask.  Masks are visited grouped by e_last (the row after
+// the last low cut: x in [2^(e-1), 2^e) has e_last = e), so the straddling stage
+// [e_last, c_h) folded with the high stages is one register set per group.  Per mask only
+// the low-table entry is combined and the key formed with the trees of eval_partition
+// (FB = maxF + maxB, delta maxY and memI are exact in double, so they equal the int64
+// forms converted); memory feasibility is the threshold memI <= mem_max.  Only the
+// smallest high word of the block's keys is kept; a block that may hold a candidate is
+// re-evaluated mask by mask through eval_partition (offers).
+template <int FAM>
+__device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                                 uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
+                                 const LowD *lowtab, const int8_t *tier_by_n) {
+    BlkCtx C = make_blk(w, smem, memo);
+    const View &v = C.v;
+    const ModelHdr *M = v.M;
+    const ImgHdr *H = v.H;
+    const int lane = threadIdx.x & 31;
+    const int G = M->G;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+    const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+    const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    const uint64_t span = C.Q << kLowBits;
+    const uint64_t nblk = (w.hi - w.lo) / span;
+    const uint64_t c = w.steps;
+    const uint64_t blk0 = (tile * 32 + lane) * c;
+    const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
+    const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
+    const int64_t delta = H->delta;
+    const double dd = i2d(delta);
+    const int64_t Sg = C.Sv[0];
+    double cap_memo = CUDART_NAN, mem_max_d = -1.0;
+    Lane L;
+    if (nmine) decode(v, w.lo + blk0 * span, L, cuts, kThreads);
+    for (uint32_t it = 0; it < iters; it++) {
+        const bool act = it < nmine;
+        const uint64_t hi_mask = L.part & ~(((uint64_t)1 << kLowBits) - 1);
+        int64_t hF = 0, hB = 0, hU = 0, hM = 0, hY = 0;
+        int c_h = G;
+        int hpop = 0;
+        int64_t b = 1;
+        const LowD *lt = lowtab;
+        int hmin = 0x7fffffff;
+        uint32_t nok = 0;
+        if (act) {
+            b = at<int64_t>(v.img, v.S->off_b)[L.d[D_B]];
+            lt = lowtab + (size_t)L.d[D_B] * (1 << kLowBits);
+            uint64_t m = hi_mask;
+            hpop = __popcll(m);
+            if (m) {
+                c_h = __ffsll((long long)m);
+                m &= m - 1;
+                int beg = c_h;
+                hY = Y[c_h - 1];
+                for (;;) {
+                    const int end = m ? __ffsll((long long)m) : G;
+                    m &= m - 1;
+                    hF = max(hF, PF[end] - PF[beg]);
+                    hB = max(hB, PB[end] - PB[beg]);
+                    hU = max(hU, PU[end] - PU[beg]);
+                    hM = max(hM, 2 * b * (PX[end] - PX[beg]) + 2 * (PW[end] - PW[beg]) + (PI[end] - PI[beg]));
+                    if (end == G) break;
+                    hY = max(hY, Y[end - 1]);
+                    beg = end;
+                }
+            }
+            const double cap = at<double>(v.img, v.S->off_cap)[L.d[D_CAP]];
+            const double R = at<double>(v.img, v.S->off_flops)[L.d[D_FLOPS]];
+            if (R != C.R_memo) {
+                C.R_memo = R;
+                C.tau = ddiv(1.0, R);
+            }
+            if (!(cap == cap_memo)) {
+                cap_memo = cap;
+                mem_max_d = i2d(mem_threshold(H, cap));
+            }
+            const double tau = C.tau;
+            const double *mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
+            const double bS = mrow[0], I = mrow[C.nS];
+            const bool seg_ok = Sg >= 1 && Sg <= b;
+            const double hFd = i2d(hF), hBd = i2d(hB), hUd = i2d(hU), hMd = i2d(hM), hYd = i2d(hY);
+            const double a0 = C.alpha_tab[0], b0 = C.beta_tab[0];
+            const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
+            for (int e = 0; e <= kLowBits; e++) {
+                const int x0 = e ? 1 << (e - 1) : 0, x1 = e ? 1 << e : 1;
+                const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
+                const double TU = fmax(i2d(cU - PU[e]), hUd);
+                const double TM = fmax(i2d(2 * b * (cX - PX[e]) + 2 * (cW - PW[e]) + (cI - PI[e])), hMd);
+#pragma unroll 2
+                for (int x = x0; x < x1; x++) {
+                    const LowD q = lt[x];
+                    const double maxF = fmax(q.F, TF), maxB = fmax(q.B, TB), maxU = fmax(q.U, TU);
+                    const double memI = fmax(q.M, TM), maxY = fmax(q.Y, hYd);
+                    const int ns = q.pop + hpop + 1;
+                    const int tsr = tier_by_n[ns];
+                    const bool feas = seg_ok && tsr >= 0 && memI <= mem_max_d;
+                    const double cseg = dmul(i2d((int64_t)ns + Sg - 1), bS);
+                    const double comp = dadd(dmul(dmul(cseg, dadd(maxF, maxB)), tau), dmul(maxU, tau));
+                    const double ppc = ns > 1 ? i2d(2 * ((int64_t)ns + Sg - 2)) : 0.0;
+                    const double pps = ns > 1 ? dmul(bS, dmul(dd, maxY)) : 0.0;
+                    const double av = tsr > 0 ? C.alpha_tab[tsr] : a0, bv = tsr > 0 ? C.beta_tab[tsr] : b0;
+                    const double key = dmul(dadd(comp, dmul(ppc, dadd(av, dmul(pps, bv)))), I);
+                    nok += feas ? 1u : 0u;
+                    hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
+                }
+            }
+        }
+        cnt += nok;
+        const bool maybe = act && hmin <= __double2hiint(tk.adm);
+        if (__any_sync(0xffffffffu, maybe)) {
+            const uint64_t gbase = v.S->offset + w.lo + (blk0 + it) * span;
+            for (uint32_t x = 0; x < (1u << kLowBits); x++) {
+                StageT st;
+                int64_t ns = 1;
+                if (maybe) {
+                    const LowD q = lt[x];
+                    const int beg = q.e_last;
+                    st.maxF = max(max((int64_t)__double2ll_rn(q.F), PF[c_h] - PF[beg]), hF);
+                    st.maxB = max(max((int64_t)__double2ll_rn(q.B), PB[c_h] - PB[beg]), hB);
+                    st.maxU = max(max((int64_t)__double2ll_rn(q.U), PU[c_h] - PU[beg]), hU);
+                    st.maxW = 0;   // pd only
+                    st.sumY = 0;   // layer-pure only
+                    st.memI = max(max((int64_t)__double2ll_rn(q.M),
+                                      2 * b * (PX[c_h] - PX[beg]) + 2 * (PW[c_h] - PW[beg]) + (PI[c_h] - PI[beg])),
+                                  hM);
+                    st.maxY = max((int64_t)__double2ll_rn(q.Y), hY);
+                    ns = q.pop + hpop + 1;
+                }
+                eval_partition<FAM, false>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
+            }
+        }
+        tk.refresh();
+        if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 256
+    }
 }
 
 template <int FAM>
@@ -1574,9 +1723,6 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
     Lane L;
     if (nmine) decode(v, w.lo + blk0 * span, L, cuts, kThreads);
-    const bool screen = FAM == PARADL_PIPELINE && C.Q == 1;
-    double cap_memo = CUDART_NAN;
-    int64_t mem_max = -1;
     for (uint32_t it = 0; it < iters; it++) {
         const bool act = it < nmine;
         // high part of this block: stages after the first high cut
@@ -1620,81 +1766,24 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
             }
         }
         const uint64_t gbase = v.S->offset + w.lo + (blk0 + it) * span;
-        bool maybe = act;
-        if (screen) {
-            // screened block (pipeline, one configuration per mask): every key with the trees
-            // of eval_partition, only the smallest high word kept; memory feasibility by the
-            // integer threshold memI <= mem_max (gamma (delta memI) is monotone in memI)
-            int hmin = 0x7fffffff;
+        for (uint32_t x = 0; x < (1u << kLowBits); x++) {
+            StageT st;
+            int64_t ns = 1;
             if (act) {
-                const ImgHdr *H = v.H;
-                const double cap = at<double>(v.img, v.S->off_cap)[L.d[D_CAP]];
-                const double R = at<double>(v.img, v.S->off_flops)[L.d[D_FLOPS]];
-                if (R != C.R_memo) {
-                    C.R_memo = R;
-                    C.tau = ddiv(1.0, R);
-                }
-                if (!(cap == cap_memo)) {
-                    cap_memo = cap;
-                    mem_max = mem_threshold(H, cap);
-                }
-                const double tau = C.tau;
-                const double *mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
-                const double bS = mrow[0], I = mrow[C.nS];
-                const int64_t Sg = C.Sv[0];
-                const bool seg_ok = Sg >= 1 && Sg <= b;
-                const int64_t delta = H->delta;
-                const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
-                uint32_t nok = 0;
-#pragma unroll 2
-                for (uint32_t x = 0; x < (1u << kLowBits); x++) {
-                    const LowE e = lt[x];
-                    const int beg = e.e_last;
-                    const int64_t maxF = max(max(e.F, cF - PF[beg]), hF);
-                    const int64_t maxB = max(max(e.B, cB - PB[beg]), hB);
-                    const int64_t maxU = max(max(e.U, cU - PU[beg]), hU);
-                    const int64_t memI = max(max(e.memI, 2 * b * (cX - PX[beg]) + 2 * (cW - PW[beg]) + (cI - PI[beg])), hM);
-                    const int64_t maxY = max(e.maxY, hY);
-                    const int64_t ns = e.pop + hpop + 1;
-                    const int tsr = tier_of(H, ns);
-                    const int ts = max(tsr, 0);
-                    const bool feas = seg_ok && tsr >= 0 && memI <= mem_max;
-                    const double cseg = dmul(i2d(ns + Sg - 1), bS);
-                    const double comp = dadd(dmul(dmul(cseg, i2d(maxF + maxB)), tau), dmul(i2d(maxU), tau));
-                    const double ppc = ns > 1 ? i2d(2 * (ns + Sg - 2)) : 0.0;
-                    const double pps = ns > 1 ? dmul(bS, i2d(delta * maxY)) : 0.0;
-                    const double key =
-                        dmul(dadd(comp, dmul(ppc, dadd(C.alpha_tab[ts], dmul(pps, C.beta_tab[ts])))), I);
-                    nok += feas ? 1u : 0u;
-                    hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
-                }
-                cnt += nok;
+                const LowE e = lt[x];
+                const int beg = e.e_last;
+                const int64_t F = PF[c_h] - PF[beg], Bw = PB[c_h] - PB[beg], U = PU[c_h] - PU[beg];
+                const int64_t Wt = PW[c_h] - PW[beg], XY = PX[c_h] - PX[beg], BI = PI[c_h] - PI[beg];
+                st.maxF = max(max(e.F, F), hF);
+                st.maxB = max(max(e.B, Bw), hB);
+                st.maxU = max(max(e.U, U), hU);
+                st.maxW = max(max(e.W, Wt), hW);
+                st.memI = max(max(e.memI, 2 * b * XY + 2 * Wt + BI), hM);
+                st.maxY = max(e.maxY, hY);
+                st.sumY = e.sumY + hS;
+                ns = e.pop + hpop + 1;
             }
-            maybe = act && hmin <= __double2hiint(tk.adm);
-        }
-        if (!screen || __any_sync(0xffffffffu, maybe)) {
-            for (uint32_t x = 0; x < (1u << kLowBits); x++) {
-                StageT st;
-                int64_t ns = 1;
-                if (maybe) {
-                    const LowE e = lt[x];
-                    const int beg = e.e_last;
-                    const int64_t F = PF[c_h] - PF[beg], Bw = PB[c_h] - PB[beg], U = PU[c_h] - PU[beg];
-                    const int64_t Wt = PW[c_h] - PW[beg], XY = PX[c_h] - PX[beg], BI = PI[c_h] - PI[beg];
-                    st.maxF = max(max(e.F, F), hF);
-                    st.maxB = max(max(e.B, Bw), hB);
-                    st.maxU = max(max(e.U, U), hU);
-                    st.maxW = max(max(e.W, Wt), hW);
-                    st.memI = max(max(e.memI, 2 * b * XY + 2 * Wt + BI), hM);
-                    st.maxY = max(e.maxY, hY);
-                    st.sumY = e.sumY + hS;
-                    ns = e.pop + hpop + 1;
-                }
-                if (screen)
-                    eval_partition<FAM, false>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
-                else
-                    eval_partition<FAM>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
-            }
+            eval_partition<FAM>(C, act, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
         }
         tk.refresh();
         if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 256
@@ -1704,6 +1793,12 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
 // Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
 // with the same fp64 operations compute_mid uses, and the low-bit stage tables of mode 2.
 __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base, LowE *low_base) {
+    {
+        SmemExtra *ex = reinterpret_cast<SmemExtra *>(smem + a.img_bytes);
+        const ImgHdr *H = at<ImgHdr>(smem, 0);
+        for (int n = threadIdx.x; n < PARADL_MAX_STAGES + 8; n += blockDim.x)
+            ex->tier_by_n[n] = (int8_t)(n >= 1 ? tier_of(H, n) : 0);
+    }
     for (int wi = 0; wi < a.n_work; wi++) {
         const WorkItem &w = a.work[wi];
         if (w.mode == 0) continue;
@@ -1784,7 +1879,20 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 }
                 L.e_last = beg;
                 L.pop = __popc(x);
-                (low_base + w.low_off)[e] = L;
+                if (w.flags & kWorkMaskD) {
+                    LowD d;
+                    d.F = i2d(L.F);
+                    d.B = i2d(L.B);
+                    d.U = i2d(L.U);
+                    d.M = i2d(L.memI);
+                    d.Y = i2d(L.maxY);
+                    d.pop = L.pop;
+                    d.e_last = L.e_last;
+                    d.pad_[0] = d.pad_[1] = 0.0;
+                    reinterpret_cast<LowD *>(low_base + w.low_off)[e] = d;
+                } else {
+                    (low_base + w.low_off)[e] = L;
+                }
             }
         }
     }
@@ -1824,8 +1932,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         const WorkItem &w = a.work[wi];
         if (BLK == 1)
             tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, dtab);
-        else if (BLK == 2)
-            tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
+        else if (BLK == 2) {
+            if (FAM == PARADL_PIPELINE && (w.flags & kWorkMaskD))
+                tile_body_mask_d<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
+                                      reinterpret_cast<const LowD *>(lowtab + w.low_off), ex->tier_by_n);
+            else
+                tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
+        }
         else
             tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
     }

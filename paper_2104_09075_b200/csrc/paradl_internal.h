@@ -22,6 +22,7 @@ constexpr int kMaxWork = 8;              // work items per sweep launch (kernel 
 constexpr int kMaxModelsPerSweep = 8;
 constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kWorkMaskD = 1u;
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 
@@ -92,7 +93,8 @@ struct WorkItem {
     uint64_t inc_part;
     const HaloEntry *halo;         // spatial / ds: [n_dims][n_Ls] table (device global), else null
     uint32_t memo_off, memo_n;     // mode 1/2: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
-    uint32_t low_off, pad2;        // mode 2: index of its [n_b][256] low-bit stage table (LowE units)
+    uint32_t low_off, flags;       // mode 2: index of its [n_b][256] low-bit stage table (LowE units);
+                                   // flags: kWorkMaskD = screened pipeline masks, stage terms as exact doubles
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
