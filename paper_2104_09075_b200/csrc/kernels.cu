@@ -1536,7 +1536,8 @@ static_assert(sizeof(LowE) == 64, "LowE layout");
 struct LowD {
     double F, B, U, M, Y;
     int32_t pop, e_last;
-    double pad_[2];
+    double Ypp;   // pp_s of the low stages: b/S (delta maxY), monotone in maxY
+    double pad_;
 };
 static_assert(sizeof(LowD) == 64, "LowD layout");
 
@@ -1643,28 +1644,31 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
             const double *mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
             const double bS = mrow[0], I = mrow[C.nS];
             const bool seg_ok = Sg >= 1 && Sg <= b;
-            const double hFd = i2d(hF), hBd = i2d(hB), hUd = i2d(hU), hMd = i2d(hM), hYd = i2d(hY);
-            const double a0 = C.alpha_tab[0], b0 = C.beta_tab[0];
+            const double hFd = i2d(hF), hBd = i2d(hB), hUd = i2d(hU), hMd = i2d(hM);
+            const double hpps = dmul(bS, dmul(dd, i2d(hY)));
+            const uint32_t nb = v.S->radix[D_B];
+            const double *cs_n = C.memo + (size_t)nb * (C.nS + C.nD) + (size_t)L.d[D_B] * kMaskTabN;
+            const double *pc_n = C.memo + (size_t)nb * (C.nS + C.nD) + (size_t)nb * kMaskTabN;
+            const double *aw_n = pc_n + kMaskTabN, *bw_n = aw_n + kMaskTabN;
             const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
             for (int e = 0; e <= kLowBits; e++) {
                 const int x0 = e ? 1 << (e - 1) : 0, x1 = e ? 1 << e : 1;
                 const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
                 const double TU = fmax(i2d(cU - PU[e]), hUd);
                 const double TM = fmax(i2d(2 * b * (cX - PX[e]) + 2 * (cW - PW[e]) + (cI - PI[e])), hMd);
+                // memI = max(low, T) <= mem_max  <=>  both are
+                const bool grp_ok = seg_ok && TM <= mem_max_d;
 #pragma unroll 2
                 for (int x = x0; x < x1; x++) {
                     const LowD q = lt[x];
-                    const double maxF = fmax(q.F, TF), maxB = fmax(q.B, TB), maxU = fmax(q.U, TU);
-                    const double memI = fmax(q.M, TM), maxY = fmax(q.Y, hYd);
+                    // maxima of non-NaN values as compare-select (fmax adds NaN handling); pp_s is
+                    // a monotone function of maxY, so it is the max of the two precomputed parts
+                    const double maxF = q.F > TF ? q.F : TF, maxB = q.B > TB ? q.B : TB;
+                    const double maxU = q.U > TU ? q.U : TU, pps = q.Ypp > hpps ? q.Ypp : hpps;
                     const int ns = q.pop + hpop + 1;
-                    const int tsr = tier_by_n[ns];
-                    const bool feas = seg_ok && tsr >= 0 && memI <= mem_max_d;
-                    const double cseg = dmul(i2d((int64_t)ns + Sg - 1), bS);
-                    const double comp = dadd(dmul(dmul(cseg, dadd(maxF, maxB)), tau), dmul(maxU, tau));
-                    const double ppc = ns > 1 ? i2d(2 * ((int64_t)ns + Sg - 2)) : 0.0;
-                    const double pps = ns > 1 ? dmul(bS, dmul(dd, maxY)) : 0.0;
-                    const double av = tsr > 0 ? C.alpha_tab[tsr] : a0, bv = tsr > 0 ? C.beta_tab[tsr] : b0;
-                    const double key = dmul(dadd(comp, dmul(ppc, dadd(av, dmul(pps, bv)))), I);
+                    const bool feas = grp_ok && q.M <= mem_max_d && tier_by_n[ns] >= 0;
+                    const double comp = dadd(dmul(dmul(cs_n[ns], dadd(maxF, maxB)), tau), dmul(maxU, tau));
+                    const double key = dmul(dadd(comp, dmul(pc_n[ns], dadd(aw_n[ns], dmul(pps, bw_n[ns])))), I);
                     nok += feas ? 1u : 0u;
                     hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
                 }
@@ -1839,6 +1843,26 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 }
             }
         }
+        if (w.mode == 2 && (w.flags & kWorkMaskD)) {
+            // screened masks (n_S = 1, one alpha/beta row): per stage count n the same fp64
+            // values eval_partition forms: cseg = (n + S - 1) (b / S), pp_c, and alpha/beta of
+            // tier_of(n) (0 when no tier holds n stages; such masks are infeasible)
+            const uint32_t nb = S->radix[D_B];
+            double *cs = tab + nrow, *pc = cs + nb * kMaskTabN, *aw = pc + kMaskTabN, *bw = aw + kMaskTabN;
+            const int64_t Sg = Sv[0];
+            const double *al = at<double>(v.img, S->off_alpha), *be = at<double>(v.img, S->off_beta);
+            for (uint32_t e = threadIdx.x; e < (nb + 3) * kMaskTabN; e += blockDim.x) {
+                const uint32_t r = e / kMaskTabN, n = e - r * kMaskTabN;
+                if (r < nb) {
+                    cs[e] = dmul(i2d((int64_t)n + Sg - 1), ddiv(i2d(bv[r]), i2d(Sg)));
+                } else if (r == nb) {
+                    pc[n] = i2d(n > 1 ? 2 * ((int64_t)n + Sg - 2) : 0);
+                } else {
+                    const int t = n >= 1 ? tier_of(v.H, n) : -1;
+                    (r == nb + 1 ? aw : bw)[n] = t >= 0 ? (r == nb + 1 ? al : be)[t] : 0.0;
+                }
+            }
+        }
         for (uint32_t e = threadIdx.x; e < nrow; e += blockDim.x) {
             const uint32_t ib = e / (nS + nD), j = e - ib * (nS + nD);
             const int64_t b = bv[ib];
@@ -1888,7 +1912,8 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                     d.Y = i2d(L.maxY);
                     d.pop = L.pop;
                     d.e_last = L.e_last;
-                    d.pad_[0] = d.pad_[1] = 0.0;
+                    d.Ypp = dmul(ddiv(i2d(b), i2d(Sv[0])), dmul(i2d(v.H->delta), d.Y));
+                    d.pad_ = 0.0;
                     reinterpret_cast<LowD *>(low_base + w.low_off)[e] = d;
                 } else {
                     (low_base + w.low_off)[e] = L;
@@ -1913,7 +1938,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     WarpTopK tk;
     tk.init(a.k, DENSE ? nullptr : a.gbound);
     unsigned long long cnt = 0;
-    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
     double *memo = reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra));
     LowE *lowtab = reinterpret_cast<LowE *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes);
     double *dtab = a.dtab_bytes ? reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes +

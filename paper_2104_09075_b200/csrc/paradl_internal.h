@@ -23,6 +23,7 @@ constexpr int kMaxModelsPerSweep = 8;
 constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kWorkMaskD = 1u;
+constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the screened mask path (n <= 64)
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 
