@@ -664,8 +664,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         const uint64_t n_stage = (h.part_mode == PARADL_PART_COMB ? (uint64_t)h.s_max : (uint64_t)h.G) + 1;
         const uint64_t ctab_n = fam == PARADL_PD ? n_stage * (h.radix[D_DIMS] + 1) : 0;
         const bool mask2 = h.part_mode == PARADL_PART_MASK && h.G >= 10 && h.radix[D_B] <= 2;
-        // screened pipeline masks: per stage count n <= 64 the tables cseg[n_b][65], ppc, alpha, beta[65]
-        const uint64_t maskd_n = (mask2 && fam == PARADL_PIPELINE && Q == 1) ? (h.radix[D_B] + 3ull) * kMaskTabN : 0;
+        // screened pipeline masks: per (b, stage count n <= 64) {cseg, pp_c, alpha, beta} (NTab)
+        const uint64_t maskd_n = (mask2 && fam == PARADL_PIPELINE && Q == 1) ? h.radix[D_B] * 4ull * kMaskTabN : 0;
         const uint64_t memo_n =
             (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]) + ctab_n + (ctab_n + 1) / 2 + maskd_n;
         const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22))

@@ -998,7 +998,7 @@ __device__ void bitonic_sort_smem(paradl_hit *x, int n) {
     }
 }
 
-struct SmemExtra {
+struct __align__(16) SmemExtra {
     uint16_t cuts[kMaxCuts][kThreads];
     paradl_hit lists[kWarps][PARADL_MAX_TOPK];
     int8_t tier_by_n[PARADL_MAX_STAGES + 8];   // tier_of(n), n <= 64 (mask stage counts)
@@ -1533,11 +1533,15 @@ struct LowE {
 };
 static_assert(sizeof(LowE) == 64, "LowE layout");
 // the same low-bit table as exact doubles (kWorkMaskD: every stage term < 2^53)
-struct LowD {
-    double F, B, U, M, Y;
-    int32_t pop, e_last;
+struct __align__(16) LowD {
+    double F, B, U, M;
     double Ypp;   // pp_s of the low stages: b/S (delta maxY), monotone in maxY
-    double pad_;
+    int32_t pop, e_last;
+    double Y, pad_;
+};
+// per (b, stage count n) values of the screened mask path
+struct __align__(16) NTab {
+    double cseg, ppc, aw, bw;
 };
 static_assert(sizeof(LowD) == 64, "LowD layout");
 
@@ -1647,9 +1651,8 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
             const double hFd = i2d(hF), hBd = i2d(hB), hUd = i2d(hU), hMd = i2d(hM);
             const double hpps = dmul(bS, dmul(dd, i2d(hY)));
             const uint32_t nb = v.S->radix[D_B];
-            const double *cs_n = C.memo + (size_t)nb * (C.nS + C.nD) + (size_t)L.d[D_B] * kMaskTabN;
-            const double *pc_n = C.memo + (size_t)nb * (C.nS + C.nD) + (size_t)nb * kMaskTabN;
-            const double *aw_n = pc_n + kMaskTabN, *bw_n = aw_n + kMaskTabN;
+            const NTab *nt = reinterpret_cast<const NTab *>(C.memo + (size_t)nb * (C.nS + C.nD)) +
+                             (size_t)L.d[D_B] * kMaskTabN;
             const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
             for (int e = 0; e <= kLowBits; e++) {
                 const int x0 = e ? 1 << (e - 1) : 0, x1 = e ? 1 << e : 1;
@@ -1660,15 +1663,17 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
                 const bool grp_ok = seg_ok && TM <= mem_max_d;
 #pragma unroll 2
                 for (int x = x0; x < x1; x++) {
-                    const LowD q = lt[x];
+                    const double2 *qp = reinterpret_cast<const double2 *>(lt + x);
+                    const double2 qFB = qp[0], qUM = qp[1], qY = qp[2];
                     // maxima of non-NaN values as compare-select (fmax adds NaN handling); pp_s is
                     // a monotone function of maxY, so it is the max of the two precomputed parts
-                    const double maxF = q.F > TF ? q.F : TF, maxB = q.B > TB ? q.B : TB;
-                    const double maxU = q.U > TU ? q.U : TU, pps = q.Ypp > hpps ? q.Ypp : hpps;
-                    const int ns = q.pop + hpop + 1;
-                    const bool feas = grp_ok && q.M <= mem_max_d && tier_by_n[ns] >= 0;
-                    const double comp = dadd(dmul(dmul(cs_n[ns], dadd(maxF, maxB)), tau), dmul(maxU, tau));
-                    const double key = dmul(dadd(comp, dmul(pc_n[ns], dadd(aw_n[ns], dmul(pps, bw_n[ns])))), I);
+                    const double maxF = qFB.x > TF ? qFB.x : TF, maxB = qFB.y > TB ? qFB.y : TB;
+                    const double maxU = qUM.x > TU ? qUM.x : TU, pps = qY.x > hpps ? qY.x : hpps;
+                    const int ns = __double2loint(qY.y) + hpop + 1;   // LowD.pop
+                    const NTab tq = nt[ns];
+                    const bool feas = grp_ok & (qUM.y <= mem_max_d) & (tier_by_n[ns] >= 0);
+                    const double comp = dadd(dmul(dmul(tq.cseg, dadd(maxF, maxB)), tau), dmul(maxU, tau));
+                    const double key = dmul(dadd(comp, dmul(tq.ppc, dadd(tq.aw, dmul(pps, tq.bw)))), I);
                     nok += feas ? 1u : 0u;
                     hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
                 }
@@ -1848,19 +1853,18 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
             // values eval_partition forms: cseg = (n + S - 1) (b / S), pp_c, and alpha/beta of
             // tier_of(n) (0 when no tier holds n stages; such masks are infeasible)
             const uint32_t nb = S->radix[D_B];
-            double *cs = tab + nrow, *pc = cs + nb * kMaskTabN, *aw = pc + kMaskTabN, *bw = aw + kMaskTabN;
+            NTab *nt = reinterpret_cast<NTab *>(tab + nrow);
             const int64_t Sg = Sv[0];
             const double *al = at<double>(v.img, S->off_alpha), *be = at<double>(v.img, S->off_beta);
-            for (uint32_t e = threadIdx.x; e < (nb + 3) * kMaskTabN; e += blockDim.x) {
+            for (uint32_t e = threadIdx.x; e < nb * kMaskTabN; e += blockDim.x) {
                 const uint32_t r = e / kMaskTabN, n = e - r * kMaskTabN;
-                if (r < nb) {
-                    cs[e] = dmul(i2d((int64_t)n + Sg - 1), ddiv(i2d(bv[r]), i2d(Sg)));
-                } else if (r == nb) {
-                    pc[n] = i2d(n > 1 ? 2 * ((int64_t)n + Sg - 2) : 0);
-                } else {
-                    const int t = n >= 1 ? tier_of(v.H, n) : -1;
-                    (r == nb + 1 ? aw : bw)[n] = t >= 0 ? (r == nb + 1 ? al : be)[t] : 0.0;
-                }
+                const int t = n >= 1 ? tier_of(v.H, n) : -1;
+                NTab q;
+                q.cseg = dmul(i2d((int64_t)n + Sg - 1), ddiv(i2d(bv[r]), i2d(Sg)));
+                q.ppc = i2d(n > 1 ? 2 * ((int64_t)n + Sg - 2) : 0);
+                q.aw = t >= 0 ? al[t] : 0.0;
+                q.bw = t >= 0 ? be[t] : 0.0;
+                nt[e] = q;
             }
         }
         for (uint32_t e = threadIdx.x; e < nrow; e += blockDim.x) {
