@@ -929,11 +929,12 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
 #pragma unroll
             for (int i = 0; i < M; i++) key[q * M + i] = dmul(combine<FAM>(m, av, sv[i]), m.I);
         }
-        const double th = tk.adm;
-        unsigned b = 0;
+        // admission screen on the high words (integer min; key <= adm implies hi(key) <=
+        // hi(adm) for non-negative doubles), one vote per R*M keys; offer() is exact
+        int hk = __double2hiint(key[0]);
 #pragma unroll
-        for (int i = 0; i < R * M; i++) b |= __ballot_sync(full, key[i] <= th);
-        if (b) {
+        for (int i = 1; i < R * M; i++) hk = min(hk, __double2hiint(key[i]));
+        if (__any_sync(full, hk <= __double2hiint(tk.adm))) {
 #pragma unroll
             for (int i = 0; i < R * M; i++) tk.offer(true, key[i], idx0 + 32ull * (r + i));
         }
