@@ -817,7 +817,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
             } else {
                 // >= ~8 tiles per warp for balance, but at least one whole alpha/beta block per
-                // tile (structure terms are computed once per block), 32..32768 configs per tile
+                // tile (structure terms are computed once per block), 32..131072 configs per tile
                 const SubHdr &h = P.subs[w.sub].hdr;
                 const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
                 uint64_t steps = std::max<uint64_t>(range / n_shards / (32ull * warps * 8ull), (nAB + 31) / 32);
