@@ -61,7 +61,7 @@ static int64_t nz(int32_t n) { return n > 0 ? n : 1; }
 static int part_count(const or_model *m, const or_sub *s, uint64_t *out)
 {
     int fam = s->family;
-    int is_pipe = (fam == OR_PIPELINE || fam == OR_LAYERPURE || fam == OR_PD);
+    int is_pipe = (fam == OR_PIPELINE || fam == OR_LAYERPURE || fam == OR_PD || fam == OR_GPIPE);
     if (!is_pipe) {
         if (s->part_mode != OR_PART_NONE) FAIL(E_INVAL, "partition mode on a non-pipeline family");
         *out = 1;
@@ -88,8 +88,14 @@ static int sub_count(const or_model *models, int n_models, const or_system *sys,
     if (s->model < 0 || s->model >= n_models) FAIL(E_INVAL, "bad model index");
     if (s->family < 0 || s->family >= OR_N_FAMILIES) FAIL(E_INVAL, "bad family");
     if (s->n_b <= 0) FAIL(E_INVAL, "empty batch list");
-    if ((s->family == OR_SPATIAL || s->family == OR_DS) && s->n_Ls <= 0)
+    if ((s->family == OR_SPATIAL || s->family == OR_DS || s->family == OR_SPATIAL_AG) && s->n_Ls <= 0)
         FAIL(E_INVAL, "spatial family needs an Ls list");
+    if (s->family == OR_SPATIAL_AG)
+        for (int i = 0; i < s->n_Ls; i++)
+            if (s->Ls[i] < 1) FAIL(E_INVAL, "spatial_ag needs Ls >= 1");
+    if (s->family == OR_GPIPE)
+        for (int i = 0; i < s->n_S; i++)
+            if (s->S[i] < 1) FAIL(E_INVAL, "gpipe needs S >= 1");
     if (s->n_alpha > 0 && sys->n_tiers <= 0) FAIL(E_INVAL, "no tiers");
     uint64_t np;
     int rc = part_count(&models[s->model], s, &np);
@@ -536,6 +542,127 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (S < 1 || S > b) reason |= OR_R_SEGMENTS;   /* S <= B (Q9) */
         break;
     }
+    case OR_SPATIAL_AG: {
+        /* "we implement the spatial strategy for some first layers ... We then
+         * implement an Allgather to collect the full set of activations before passing
+         * it to the following layers which perform similar to the sequential
+         * implementation."  Rows [0, Ls) as the Spatial row of Table 2;
+         * rows [Ls, G) replicated on every PE (compute and activations not divided by
+         * p); one Allgather of the boundary activation y_Ls (per-PE segment B|y_Ls|/p,
+         * P:556 with Q19); GE over all weights as Spatial (Q35). */
+        int32_t split[3] = {d[1], d[2], d[3]};
+        if (d[0] != 1) FAIL(E_INVAL, "spatial_ag needs p1 == 1");
+        if (c->Ls < 1) FAIL(E_INVAL, "spatial_ag needs Ls >= 1");
+        p = (int64_t)d[1] * d[2] * d[3];
+        B = b;
+        int64_t Lp = c->Ls < m->G ? c->Ls : m->G;
+        int64_t FBp = 0, FBs = 0, XYp = 0, XYs = 0;
+        for (int64_t l = 0; l < m->G; l++) {
+            const or_layer *r = &m->rows[l];
+            if (l < Lp) { FBp += r->fw + r->bw; XYp += r->x + r->y; }
+            else        { FBs += r->fw + r->bw; XYs += r->x + r->y; }
+        }
+        int64_t BFBp, BFBs, tBXYp, tBXYs, BdY;
+        if (!mul_ok(B, FBp, &BFBp) || !mul_ok(B, FBs, &BFBs) || !mul_ok(2 * B, XYp, &tBXYp) ||
+            !mul_ok(2 * B, XYs, &tBXYs) || !mul_ok(B * delta, m->rows[Lp - 1].y, &BdY))
+            FAIL(E_OVERFLOW, "B*FB");
+        /* comp: prefix rows / p, suffix rows in full, WU in full (replicated weights) */
+        comp = ((((double)BFBp / (double)p) * tau) + (double)BFBs * tau) + (double)s.WU * tau;
+        int64_t NS, HV, bdHV;
+        reason |= spatial_terms(m, c->Ls, split, &NS, &HV);
+        if (!mul_ok(b * delta, HV, &bdHV)) FAIL(E_OVERFLOW, "b*delta*HV");
+        int t = tier_or_flag(sys, p, &reason);
+        if (p > 1)
+            halo = t < 0 ? INFINITY : 2.0 * ((double)(2 * NS) * c->alpha[t] + (double)bdHV * c->beta[t]);
+        ge = t < 0 ? INFINITY : t_allreduce(sys, p, (double)dW, (double)dW / (double)p, c->alpha[t], c->beta[t]);
+        /* Allgather of y_Ls after the prefix: (p-1)(alpha + (B delta |y_Ls| / p) beta) */
+        if (Lp < m->G && p > 1)
+            ag = t < 0 ? INFINITY : (double)(p - 1) * (c->alpha[t] + ((double)BdY / (double)p) * c->beta[t]);
+        /* memory: prefix activations / p, suffix activations in full, weights replicated */
+        mem = sys->gamma * ((double)delta * ((((double)tBXYp / (double)p + (double)tBXYs) +
+                                              (double)(2 * s.W)) + (double)s.BI));
+        break;
+    }
+    case OR_GPIPE: {
+        /* GPipe: the per-replica batch b is cut into S segments of b/S
+         * samples that flow through the s stages, forward wave then backward wave.
+         * Table 2's Layer row approximates its time "by the maximum"
+         * (P:1008); this family times the schedule itself (Q36): a discrete-event
+         * simulation of the S segments over the s stages.  Stage i forward task
+         * lasts f_i = (b/S) FW_{G_i}; it then sends y_{G_i} to stage i+1 (blocking
+         * P2P: alpha + (b/S) delta |y_{G_i}| beta), so stage i is busy
+         * f_i + c_i; the backward task lasts g_i = (b/S) BW_{G_i} plus the send of the
+         * input gradient to stage i-1 (same message size).  Backward starts when the
+         * last stage finished its forward wave (GPipe flush); each stage applies WU_{G_i}
+         * after its last backward task.  Iteration time = the last WU end. */
+        int64_t ns = c->n_stages;
+        int64_t S = c->S;
+        if (d[0] != 1) FAIL(E_INVAL, "gpipe dims must be 1");
+        if (S < 1) FAIL(E_INVAL, "gpipe needs S >= 1");
+        p = ns;
+        B = b;
+        stage_t st;
+        int rc = stage_terms(m, c, b, &st);
+        if (rc) return rc;
+        int ts = tier_or_flag(sys, ns, &reason);
+        if (ts < 0) {
+            comp = INFINITY;
+        } else {
+            double fq[OR_MAX_STAGES], gq[OR_MAX_STAGES], uq[OR_MAX_STAGES], cq[OR_MAX_STAGES];
+            double mb = (double)b / (double)S;
+            int64_t beg = 0;
+            for (int i = 0; i < ns; i++) {
+                int64_t F = 0, Bw = 0, U = 0;
+                for (int64_t l = beg; l < c->stage_end[i]; l++) {
+                    F += m->rows[l].fw;
+                    Bw += m->rows[l].bw;
+                    U += m->rows[l].wu;
+                }
+                fq[i] = (mb * (double)F) * tau;
+                gq[i] = (mb * (double)Bw) * tau;
+                uq[i] = (double)U * tau;
+                cq[i] = 0.0;
+                if (i < ns - 1)
+                    cq[i] = c->alpha[ts] + (mb * (double)(delta * m->rows[c->stage_end[i] - 1].y)) * c->beta[ts];
+                beg = c->stage_end[i];
+            }
+            /* forward wave: segment j enters stage i when stage i is free and stage i-1
+             * has delivered it (stage 0 holds the input) */
+            double freeq[OR_MAX_STAGES];
+            for (int i = 0; i < ns; i++) freeq[i] = 0.0;
+            for (int64_t j = 0; j < S; j++) {
+                double ready = 0.0;
+                for (int i = 0; i < ns; i++) {
+                    double start = freeq[i] > ready ? freeq[i] : ready;
+                    double dur = i < ns - 1 ? fq[i] + cq[i] : fq[i];
+                    freeq[i] = start + dur;
+                    ready = freeq[i];
+                }
+            }
+            double t_f = freeq[ns - 1];
+            /* backward wave, last stage first, after the flush */
+            for (int i = 0; i < ns; i++) freeq[i] = t_f;
+            for (int64_t j = 0; j < S; j++) {
+                double ready = t_f;
+                for (int i = (int)ns - 1; i >= 0; i--) {
+                    double start = freeq[i] > ready ? freeq[i] : ready;
+                    double dur = i > 0 ? gq[i] + cq[i - 1] : gq[i];
+                    freeq[i] = start + dur;
+                    ready = freeq[i];
+                }
+            }
+            /* weight update per stage after its last backward task */
+            double end = 0.0;
+            for (int i = 0; i < ns; i++) {
+                double e = freeq[i] + uq[i];
+                if (e > end) end = e;
+            }
+            comp = end;
+        }
+        mem = sys->gamma * ((double)delta * (double)st.memI);   /* Table 2 Layer row memory */
+        if (S > b) reason |= OR_R_SEGMENTS;   /* Q9 */
+        break;
+    }
     default:
         FAIL(E_INVAL, "bad family");
     }
@@ -578,6 +705,36 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
     if (fam == OR_SPATIAL || fam == OR_DS) { pc = p; pa = p; }
     if (fam == OR_FILTER || fam == OR_CHANNEL) { pc = p; pu = p; pw = p; }
     if (fam == OR_DF) { pc = p; pu = d[1]; pa = d[0]; pw = d[1]; }
+    if (fam == OR_SPATIAL_AG) {
+        /* per-row fold: rows before Ls divided by p (compute, activations), the rest in full */
+        int64_t Lp = c->Ls < m->G ? c->Ls : m->G;
+        double comp = 0.0, mem = 0.0;
+        for (int64_t l = 0; l < m->G; l++) {
+            const or_layer *r = &m->rows[l];
+            double pp = l < Lp ? (double)p : 1.0;
+            comp += ((double)B / pp) * ((double)r->fw * tau + (double)r->bw * tau);
+            mem += dl * ((2.0 * (double)B) * (double)(r->x + r->y) / pp + 2.0 * (double)r->w + (double)r->bi);
+        }
+        for (int64_t l = 0; l < m->G; l++) comp += (double)m->rows[l].wu * tau;
+        o->t_comp = comp;
+        o->mem = sys->gamma * mem;
+        if (o->t_halo != 0.0 && isfinite(o->t_halo)) {
+            int32_t split[3] = {d[1], d[2], d[3]};
+            int t = tier_of(sys, p);
+            double sum = 0.0;
+            for (int64_t l = 0; l < Lp; l++) {
+                const or_layer *r = &m->rows[l];
+                if (r->kind != OR_CONV && r->kind != OR_POOL) continue;
+                double hv = (double)(or_halo_elements(r, split, 0) + or_halo_elements(r, split, 1));
+                sum += 2.0 * c->alpha[t] + (double)b * dl * c->beta[t] * hv;
+            }
+            o->t_halo = 2.0 * sum;
+        }
+        if (o->t_fb_ag != 0.0 && isfinite(o->t_fb_ag)) {
+            int t = tier_of(sys, p);
+            o->t_fb_ag = (double)(p - 1) * (c->alpha[t] + (double)B * (double)m->rows[Lp - 1].y / (double)p * dl * c->beta[t]);
+        }
+    }
     if (fam == OR_SERIAL || fam == OR_DATA || fam == OR_SPATIAL || fam == OR_DS ||
         fam == OR_FILTER || fam == OR_CHANNEL || fam == OR_DF || fam == OR_LAYERPURE) {
         int64_t Bc = fam == OR_LAYERPURE ? b : B;
@@ -587,7 +744,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
         for (int64_t l = 0; l < m->G; l++) comp += ((double)m->rows[l].wu * tau) / (double)pu;
         o->t_comp = comp;
     }
-    if (fam != OR_PIPELINE && fam != OR_LAYERPURE && fam != OR_PD) {
+    if (fam != OR_PIPELINE && fam != OR_LAYERPURE && fam != OR_PD && fam != OR_GPIPE && fam != OR_SPATIAL_AG) {
         double mem = 0.0;
         for (int64_t l = 0; l < m->G; l++) {
             const or_layer *r = &m->rows[l];

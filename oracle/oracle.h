@@ -22,7 +22,10 @@ extern "C" {
 enum { OR_CONV = 0, OR_FC = 1, OR_POOL = 2, OR_ELEM = 3, OR_NORM = 4 };
 enum { OR_FLAG_COMM = 1, OR_FLAG_FOLDED = 4 };
 enum { OR_SERIAL = 0, OR_DATA, OR_SPATIAL, OR_FILTER, OR_CHANNEL, OR_DF, OR_DS,
-       OR_PIPELINE, OR_LAYERPURE, OR_PD, OR_N_FAMILIES };
+       OR_PIPELINE, OR_LAYERPURE, OR_PD,
+       OR_SPATIAL_AG,   /* spatial on the first Ls rows, Allgather, replicated rest (Q35) */
+       OR_GPIPE,        /* pipeline timed by the GPipe schedule itself (Q36) */
+       OR_N_FAMILIES };
 enum { OR_PART_NONE = 0, OR_PART_COMB = 1, OR_PART_MASK = 2 };
 /* infeasibility reasons (bit set) */
 enum { OR_R_SCALING = 1, OR_R_MEMORY = 2, OR_R_SPLIT = 4, OR_R_TIER = 8, OR_R_SEGMENTS = 16 };

@@ -172,6 +172,33 @@ def exact(sweep, cfg):
             al = inf if to is None else ar_exact(sys, p1, Fr(dl * W_), Fr(dl * W_, p1), A[to], Bt[to])
             ge = inf if (rl is None or al is None) else rl + al
         mem = mem_row(B, p, 1)
+    elif fam == W.SPATIAL_AG:
+        # spatial on rows [0, Ls), Allgather of y_Ls, rows [Ls, G) replicated (Q35)
+        split = (d1, d2, d3)
+        p = d1 * d2 * d3
+        B = b
+        Lp = min(cfg["Ls"], len(L))
+        comp = (sum(Fr(B, p) * (r.fw + r.bw) * tau for r in L[:Lp])
+                + sum(B * (r.fw + r.bw) * tau for r in L[Lp:]) + sum(r.wu for r in L) * tau)
+        Sp = [r for r in L[:Lp] if r.kind in (M.CONV, M.POOL)]
+        for r in Sp:
+            for a in range(3):
+                if split[a] <= 1:
+                    continue
+                if split[a] > r.X[a]:
+                    reason |= R_SCALING
+                h = r.K[a] // 2
+                if _ceil(r.X[a], split[a]) < h or _ceil(r.Y[a], split[a]) < h:
+                    reason |= R_SPLIT
+        t = tier(p)
+        if p > 1:
+            halo = inf if t is None else 2 * sum(
+                2 * A[t] + b * dl * Bt[t] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
+            if Lp < len(L):
+                ag = inf if t is None else (p - 1) * (A[t] + Fr(B * L[Lp - 1].y, p) * dl * Bt[t])
+        ge = inf if t is None else ar_exact(sys, p, Fr(dl * W_), Fr(dl * W_, p), A[t], Bt[t])
+        mem = gamma * dl * sum(Fr(2 * B * (r.x + r.y), p if l < Lp else 1) + 2 * r.w + r.bi
+                               for l, r in enumerate(L))
     elif fam in (W.FILTER, W.CHANNEL):
         p = p1
         B = b
@@ -223,7 +250,22 @@ def exact(sweep, cfg):
         Wg = [sum(r.w for r in g) for g in groups]
         ycut = [g[-1].y for g in groups[:-1]]
         ts = tier(s)
-        if fam == W.LAYERPURE:
+        if fam == W.GPIPE:
+            # GPipe schedule time by the identical-job flow-shop closed form (Q36): a flow
+            # shop of S identical jobs over stage times t_1..t_m finishes its last job at
+            # stage m at sum(t) + (S-1) max(t); forward stage i is busy f_i + c_i (blocking
+            # send), backward stage i is busy g_i + c_{i-1}, all backward jobs are released
+            # at the forward makespan, and stage i applies WU after its last backward job.
+            mb = Fr(b, S)
+            if ts is None:
+                comp = inf
+            else:
+                c = [A[ts] + mb * dl * y * Bt[ts] for y in ycut] + [Fr(0)]
+                d = [mb * FWg[i] + c[i] for i in range(s)]
+                e = [mb * BWg[i] + (c[i - 1] if i > 0 else 0) for i in range(s)]
+                t_f = sum(d) + (S - 1) * max(d)
+                comp = max(t_f + sum(e[i:]) + (S - 1) * max(e[i:]) + WUg[i] for i in range(s))
+        elif fam == W.LAYERPURE:
             comp = comp_row(b, 1, 1)
             if s > 1:
                 p2p = inf if ts is None else 2 * sum(A[ts] + dl * b * y * Bt[ts] for y in ycut)
@@ -339,6 +381,10 @@ def buffer_bytes(sweep, cfg):
     elif fam in (W.SPATIAL, W.DS):
         p2 = d1 * d2 * d3
         tot = sum(layer_bufs(r, b * p1, p1 * p2, 1) for r in L)     # spatial shard of the group batch
+    elif fam == W.SPATIAL_AG:
+        p2 = d1 * d2 * d3
+        Lp = min(cfg["Ls"], len(L))
+        tot = sum(layer_bufs(r, b, p2 if l < Lp else 1, 1) for l, r in enumerate(L))   # prefix sharded
     elif fam in (W.FILTER, W.CHANNEL):
         tot = sum(layer_bufs(r, b, 1, p1) for r in L)               # full activations, w/p
     elif fam == W.DF:

@@ -302,6 +302,139 @@ def test_gpipe_schedule_vs_closed_form(oracle_mod):
             assert des >= S * Fr(B, S) * (max(f) + max(g)) / 2
 
 
+# ------------------------------------------------------------ GPipe schedule family (Q36)
+def test_gpipe_family_equals_event_simulation(oracle_mod):
+    """No communication (alpha = beta = 0) and no WU: the family's time is the makespan of
+    brute.gpipe_makespan, an independent discrete-event schedule.  Small
+    integer stage times and R = 1 keep every fp64 value exact, so equality is exact."""
+    rng = random.Random(11)
+    for trial in range(150):
+        s = rng.choice([1, 2, 3, 4, 5])
+        S = rng.choice([1, 2, 3, 4, 8])
+        B = S * rng.choice([1, 2, 3])
+        f = [rng.randint(1, 9) for _ in range(s)]
+        g = [rng.randint(1, 9) for _ in range(s)]
+        rows = [toys.row(fw=f[i], bw=g[i]) for i in range(s)]
+        m = toys.model(rows, D=B)
+        pr = _one(oracle_mod, m, toys.system(R=1.0),
+                  W.SubSweep(W.GPIPE, b=[B], S=[S], part_mode=W.PART_COMB, s_min=s, s_max=s,
+                             alpha=[[0.0]], beta=[[0.0]]))
+        des = brute.gpipe_makespan([Fr(v) for v in f], [Fr(v) for v in g], S, Fr(B, S))
+        assert Fr(pr.t_comp) == des and pr.t_iter == pr.t_comp
+        assert pr.t_p2p == 0.0 and pr.t_ge == 0.0
+
+
+def test_gpipe_equal_stages_reduce_to_table2_row(oracle_mod):
+    """Equal stages (compute, WU and boundary message): the schedule time equals Table 2's
+    Layer row exactly in rationals, (s+S-1)(b/S)(FW+BW) + WU + 2(s+S-2)(alpha +
+    (b/S) delta y beta); unequal stages: the row is an upper bound (P:1008 'approximated by
+    the maximum', Q34) and S segments of the slowest stage a lower bound."""
+    rng = random.Random(12)
+    for trial in range(120):
+        s = rng.choice([1, 2, 3, 4, 6, 8])
+        S = rng.choice([1, 2, 4, 8])
+        b = S * rng.choice([1, 2, 4])
+        equal = trial < 50
+        f = [rng.randint(1, 50) * 1000 for _ in range(s)]
+        g = [rng.randint(1, 50) * 1000 for _ in range(s)]
+        u = [rng.randint(0, 30) * 1000 for _ in range(s)]
+        y = [rng.randint(1, 40) for _ in range(s)]
+        if equal:
+            f, g, u, y = [f[0]] * s, [g[0]] * s, [u[0]] * s, [y[0]] * s
+        rows = [toys.row(fw=f[i], bw=g[i], wu=u[i], y=y[i]) for i in range(s)]
+        m = toys.model(rows, D=b)
+        A, Bt = [[rng.choice([0.0, 1e-6, 3e-5])]], [[rng.choice([0.0, 1e-9, 2e-10])]]
+        sub = dict(b=[b], S=[S], part_mode=W.PART_COMB, s_min=s, s_max=s, alpha=A, beta=Bt)
+        sysm = toys.system(R=1e9)
+        gp = _one(oracle_mod, m, sysm, W.SubSweep(W.GPIPE, **sub))
+        pl = _one(oracle_mod, m, sysm, W.SubSweep(W.PIPELINE, **sub))
+        assert gp.mem == pl.mem and gp.reason == pl.reason
+        if equal:
+            assert _rel(gp.t_iter, pl.t_iter) <= 1e-14
+        else:
+            assert gp.t_iter <= pl.t_iter * (1 + 1e-14)
+            assert gp.t_iter >= S * (b / S) * (max(f) + max(g)) / 1e9 * (1 - 1e-14)
+
+
+def test_gpipe_single_segment_is_a_chain(oracle_mod):
+    """S = 1: nothing overlaps, so the time is the chain sum f_1+c_1+...+f_s then
+    g_s+c_{s-1}+...+g_1, plus the WU of the stage that finishes last (stage 1), unless
+    a later stage's WU ends later."""
+    rng = random.Random(13)
+    for trial in range(60):
+        s = rng.choice([1, 2, 3, 4])
+        f = [rng.randint(1, 9) for _ in range(s)]
+        g = [rng.randint(1, 9) for _ in range(s)]
+        u = [rng.randint(0, 20) for _ in range(s)]
+        y = [rng.randint(1, 5) for _ in range(s)]
+        b = rng.choice([1, 2, 3])
+        rows = [toys.row(fw=f[i], bw=g[i], wu=u[i], y=y[i]) for i in range(s)]
+        m = toys.model(rows, D=b)
+        a, be = 0.5, 0.25
+        pr = _one(oracle_mod, m, toys.system(R=1.0),
+                  W.SubSweep(W.GPIPE, b=[b], S=[1], part_mode=W.PART_COMB, s_min=s, s_max=s,
+                             alpha=[[a]], beta=[[be]]))
+        dl = 1   # toys.system delta
+        c = [Fr(a) + b * dl * y[i] * Fr(be) for i in range(s - 1)]
+        t_f = sum(b * Fr(v) for v in f) + sum(c)
+        # stage i ends its backward after g_s..g_i and the sends of stages s..i (stage k
+        # sends dL/dx to stage k-1 as part of its task, so stage i's own send is included)
+        ends = [t_f + sum(b * Fr(g[k]) for k in range(i, s)) + sum(c[k - 1] for k in range(max(i, 1), s))
+                for i in range(s)]
+        want = max(ends[i] + u[i] for i in range(s))
+        assert Fr(pr.t_iter) == want
+
+
+# ------------------------------------------------------------ spatial prefix + Allgather (Q35)
+def test_spatial_ag_allgather_is_a_ring_allgather(oracle_mod):
+    """The boundary Allgather of y_Ls over p PEs with the per-PE segment B delta |y|/p
+    (Q19) equals the explicit ring allgather simulation; it vanishes at Ls >= G."""
+    rows = [toys.row(kind=M.CONV, X=(8, 8, 1), Y=(8, 8, 1), C=2, F=2, K=(3, 3, 1), x=128, y=128 + 8 * l)
+            for l in range(3)]
+    m = toys.model(rows, D=64)
+    for p in (2, 4, 8):
+        for Ls in (1, 2, 3):
+            sub = W.SubSweep(W.SPATIAL_AG, b=[4], dims=[(1, p, 1, 1)], Ls=[Ls], alpha=[[1e-6]], beta=[[1e-9]])
+            pr = _one(oracle_mod, m, toys.system(), sub)
+            if Ls >= 3:
+                assert pr.t_fb_ag == 0.0
+                continue
+            seg = Fr(4 * 1 * rows[Ls - 1].y, p)   # B = b = 4, delta = 1 (toys.system)
+            want = brute.ring_allgather_sim(p, seg, Fr(1e-6), Fr(1e-9))
+            assert _rel(pr.t_fb_ag, want) <= 1e-15
+
+
+def test_spatial_ag_limits(oracle_mod):
+    """Ls = G is the Spatial row bit for bit (no boundary, nothing replicated); p = 1 has
+    no communication and the serial compute and memory (up to rounding order); a longer
+    prefix never increases compute or memory (more rows divided by p)."""
+    for seed in range(8):
+        m = corpus.random_model(seed)
+        sysd = corpus.random_system(seed)
+        nt = len(sysd.tiers)
+        A, Bt = [[1e-5] * nt], [[1e-9] * nt]
+        dims = [(1, 1, 1, 1), (1, 2, 1, 1), (1, 2, 2, 1)]
+        sp = W.SubSweep(W.SPATIAL, b=[4], dims=dims, Ls=[m.G], alpha=A, beta=Bt)
+        ag = W.SubSweep(W.SPATIAL_AG, b=[4], dims=dims, Ls=list(range(1, m.G + 1)), alpha=A, beta=Bt)
+        se = W.SubSweep(W.SERIAL, b=[4], alpha=A, beta=Bt)
+        sw = W.Sweep([m], sysd, [sp, ag, se], "ag")
+        o = oracle_mod.OracleSweep(sw)
+        serial = _pred(o, 2, sw)
+        for d in dims:
+            x, y = _pred(o, 0, sw, dims=d), _pred(o, 1, sw, dims=d, Ls=m.G)
+            for f in ("t_comp", "t_ge", "t_fb_ag", "t_halo", "t_iter", "t_epoch", "mem", "reason"):
+                assert getattr(x, f) == getattr(y, f), (seed, d, f)
+            prev = None
+            for Ls in range(1, m.G + 1):
+                z = _pred(o, 1, sw, dims=d, Ls=Ls)
+                if d == (1, 1, 1, 1):
+                    assert z.t_ge == z.t_fb_ag == z.t_halo == 0.0
+                    assert _rel(z.t_comp, serial.t_comp) <= 1e-14 and _rel(z.mem, serial.mem) <= 1e-14
+                if prev is not None:
+                    assert z.t_comp <= prev.t_comp * (1 + 1e-15) and z.mem <= prev.mem * (1 + 1e-15)
+                prev = z
+
+
 # ------------------------------------------------------------ memory
 @pytest.mark.parametrize("seed", range(25))
 def test_memory_rows_equal_buffer_enumeration(oracle_mod, seed):

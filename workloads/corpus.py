@@ -81,7 +81,7 @@ def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:
         return A, B
 
     subs = []
-    fams = list(range(10))
+    fams = list(range(12))
     rng.shuffle(fams)
     for fam in fams:
         mi = rng.randint(0, 1)
@@ -95,21 +95,22 @@ def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:
             kw["dims"] = [(p, 1, 1, 1) for p in some([1, 2, 3, 4, 8, 16, 64, 1024])]
         elif fam == W.DF:
             kw["dims"] = [(rng.choice([1, 2, 3, 4]), rng.choice([1, 2, 4, 5]), 1, 1) for _ in range(rng.randint(1, 3))]
-        elif fam in (W.SPATIAL, W.DS):
-            kw["dims"] = [(1 if fam == W.SPATIAL else rng.choice([1, 2, 3]),
+        elif fam in W.SPATIAL_FAMILIES:
+            kw["dims"] = [(rng.choice([1, 2, 3]) if fam == W.DS else 1,
                            rng.choice([1, 2, 3, 4]), rng.choice([1, 2, 4]), rng.choice([1, 1, 2]))
                           for _ in range(rng.randint(1, 3))]
-            kw["Ls"] = some(list(range(0, m.G + 2)))
+            kw["Ls"] = some(list(range(1 if fam == W.SPATIAL_AG else 0, m.G + 2)))
         elif fam == W.PD:
             kw["dims"] = [(p, 1, 1, 1) for p in some([1, 2, 3, 4, 8])]
         if fam in W.PIPE_FAMILIES:
             kw["S"] = some([1, 2, 3, 4, 8])
-            if m.G <= 10 and rng.random() < 0.5:
+            smax_fam = 8 if fam == W.GPIPE else m.G     # GPipe: at most 8 stages (GPU limit)
+            if m.G <= min(10, smax_fam) and rng.random() < 0.5:
                 kw["part_mode"] = W.PART_MASK
             else:
                 kw["part_mode"] = W.PART_COMB
-                smin = rng.randint(1, m.G)
+                smin = rng.randint(1, min(m.G, smax_fam))
                 kw["s_min"] = smin
-                kw["s_max"] = rng.randint(smin, min(m.G, smin + 3))
+                kw["s_max"] = rng.randint(smin, min(m.G, smin + 3, smax_fam))
         subs.append(W.SubSweep(fam, **kw))
     return W.Sweep(models, sys, subs, f"rand{seed}")

@@ -16,9 +16,12 @@ from . import models as M
 
 # Strategy families (Table 2 rows P:455-516)
 SERIAL, DATA, SPATIAL, FILTER, CHANNEL, DF, DS, PIPELINE, LAYERPURE, PD = range(10)
+# SURVEY §8(f) "next" rows: spatial prefix + Allgather, GPipe schedule
+SPATIAL_AG, GPIPE = 10, 11
 FAMILY_NAMES = ["serial", "data", "spatial", "filter", "channel", "df", "ds",
-                "pipeline", "layerpure", "pd"]
-PIPE_FAMILIES = (PIPELINE, LAYERPURE, PD)
+                "pipeline", "layerpure", "pd", "spatial_ag", "gpipe"]
+PIPE_FAMILIES = (PIPELINE, LAYERPURE, PD, GPIPE)
+SPATIAL_FAMILIES = (SPATIAL, DS, SPATIAL_AG)
 
 # Partition enumeration modes
 PART_NONE, PART_COMB, PART_MASK = 0, 1, 2
