@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the SURVEY §8(f) next-row sweeps")
     return ap.parse_args()
 
 
@@ -397,6 +398,11 @@ def ours(args):
                  "copy_peak_GBps": 6538.3, "frac_of_copy_peak": ach / 6538.3}
         del t, m, bits, rs
 
+    nxt = None
+    if ws == 1 and not args.no_next:
+        nxt = next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak)
+        ctx.set_system(sweep.system)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(sweep, args.cpu_seconds)
@@ -416,6 +422,7 @@ def ours(args):
             "gpu_launches": int(gpu_launches),
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "dense": dense,
+            "next_rows": nxt,
             "result": {"argmin_idx": int(best[0, 0]) % (1 << 64), "n_feasible": n_feasible},
             "fp64_peak_inst_per_s": fp64_peak,
         }
@@ -423,6 +430,76 @@ def ours(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def gpipe_ops(s: int, S: int) -> int:
+    """FP64 instructions of one GPipe schedule evaluation: boundary costs
+    c_i = alpha + m_i beta (2 per boundary), busy times f_i + c_i and g_i + c_{i-1} (2 per
+    boundary), one add per (segment, stage) in each wave and one max per (segment > 0,
+    stage with an upstream neighbour) -- the other maxima of the event simulation are
+    provably against a smaller operand --, then s adds and s-1 maxima for the WU ends and
+    the key multiply."""
+    return 4 * (s - 1) + 2 * s * S + 2 * (s - 1) * (S - 1) + s + (s - 1) + 1
+
+
+def next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak):
+    """SURVEY §8(f) rows built this round, timed like the headline sweep (top-64 + count
+    over the whole sweep, L2 flushed before each timed launch): the GPipe schedule family
+    (f3) and the spatial prefix + Allgather family (f4)."""
+    import torch
+    out = {}
+    for name, fn in W.NEXT.items():
+        sw = fn()
+        spec = ctx.prepare(sw)
+        n = ctx.sweep_size(spec)
+        for _ in range(3):
+            ctx.topk_async(spec, 0, n, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        evs = []
+        for i in range(5):
+            flush.fill_(3)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            ctx.topk_async(spec, 0, n, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+            b_.record(stream)
+            evs.append((a_, b_))
+        torch.cuda.synchronize()
+        ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+        n_feas = int(my_cnt.item())
+        best = int(my_hits[0, 0].item()) % (1 << 64)
+        if name == "gpipe":
+            # exact algorithmic count: S varies faster than the partition and only decides
+            # SEGMENTS, so each (b, stage count) block's feasible count = feasible partitions x
+            # feasible S x alpha/beta; the per-config work depends on (s, S)
+            sb = sw.subs[0]
+            G = sw.models[0].G
+            nS, nAB = len(sb.S), len(sb.alpha) * len(sb.beta)
+            blk = [math.comb(G - 1, s - 1) for s in range(sb.s_min, sb.s_max + 1)]
+            per_b = sum(blk) * nS * nAB
+            ops = 0.0
+            for bi, b in enumerate(sb.b):
+                Sok = [S for S in sb.S if S <= b]
+                off = 0
+                for j, s in enumerate(range(sb.s_min, sb.s_max + 1)):
+                    first = bi * per_b + off * nS * nAB
+                    cnt_ = blk[j] * nS * nAB
+                    _, c = ctx.topk(spec, 1, first, cnt_)
+                    if Sok:
+                        n_pf = c / (len(Sok) * nAB)
+                        ops += n_pf * nAB * sum(gpipe_ops(s, S) for S in Sok)
+                    off += blk[j]
+            opc = ops / max(1, n_feas)
+            kern = "sweep_kernel<GPIPE,reduce>"
+        else:
+            opc = 11.0   # GE 3 + Allgather 3 + halo 4 + key 1 (alpha/beta increment, DESIGN §5.3)
+            ops = opc * n_feas
+            kern = "sweep_kernel<SPATIAL_AG,reduce>"
+        ach = ops / (ms * 1e-3) / 1e12
+        out[name] = {"workload": sw.name, "configs": n, "ms": ms, "configs_per_s": n / (ms * 1e-3),
+                     "n_feasible": n_feas, "argmin_idx": best, "kernel": kern,
+                     "roofline": {"bound": "alu", "achieved": ach, "peak": fp64_peak / 1e12,
+                                  "unit": "T fp64-pipe inst/s", "frac": ach / (fp64_peak / 1e12),
+                                  "fp64_inst_per_config": opc}}
+    return out
 
 
 def spec_model_id(ctx, spec, sub_index):

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PARADL_ABI_VERSION 1
+#define PARADL_ABI_VERSION 2
 #define PARADL_MAX_TIERS 4
 #define PARADL_MAX_STAGES 64     /* stage_end[] capacity of paradl_config */
 #define PARADL_MAX_COMB_CUTS 15  /* combination-mode partitions: s_max <= 16 */
@@ -57,11 +57,20 @@ enum { PARADL_CONV = 0, PARADL_FC = 1, PARADL_POOL = 2, PARADL_ELEM = 3, PARADL_
 enum { PARADL_FLAG_COMM = 1u, PARADL_FLAG_FOLDED = 4u };
 
 /* Strategy families (Table 2 rows). dims[4] meaning per family:
- *   SERIAL, PIPELINE, LAYERPURE: (1,1,1,1)            DATA, FILTER, CHANNEL: (p,1,1,1)
- *   DF (data+filter): (p1,p2,1,1)              SPATIAL: (1,pw,ph,pd)
- *   DS (data+spatial): (p1,pw,ph,pd)           PD (pipeline+data): (p_d,1,1,1) */
+ *   SERIAL, PIPELINE, LAYERPURE, GPIPE: (1,1,1,1)     DATA, FILTER, CHANNEL: (p,1,1,1)
+ *   DF (data+filter): (p1,p2,1,1)              SPATIAL, SPATIAL_AG: (1,pw,ph,pd)
+ *   DS (data+spatial): (p1,pw,ph,pd)           PD (pipeline+data): (p_d,1,1,1)
+ * SPATIAL_AG: spatial on the first Ls rows, then an Allgather of y_Ls and the remaining
+ *   rows replicated on every PE (the paper's implementation; Q35).
+ *   Needs Ls >= 1.
+ * GPIPE: a pipeline partition timed by the GPipe schedule itself (S segments, forward
+ *   wave then backward wave, blocking boundary sends, per-stage WU, DESIGN.md
+ *   Q36) instead of Table 2's max-stage form.  Needs s <= PARADL_GPIPE_MAX_STAGES
+ *   (COMB: s_max, MASK: G) and S >= 1. */
 enum { PARADL_SERIAL = 0, PARADL_DATA, PARADL_SPATIAL, PARADL_FILTER, PARADL_CHANNEL,
-       PARADL_DF, PARADL_DS, PARADL_PIPELINE, PARADL_LAYERPURE, PARADL_PD, PARADL_N_FAMILIES };
+       PARADL_DF, PARADL_DS, PARADL_PIPELINE, PARADL_LAYERPURE, PARADL_PD,
+       PARADL_SPATIAL_AG, PARADL_GPIPE, PARADL_N_FAMILIES };
+#define PARADL_GPIPE_MAX_STAGES 8
 
 /* Partition radix of the pipeline families (groups g_i, P:519 footnote).
  * COMB: every contiguous partition into s in [s_min, s_max] stages; s ascending, cut
@@ -170,7 +179,9 @@ typedef struct {
     int32_t stage_end[PARADL_MAX_STAGES];   /* rows in stages 1..i, last = G */
 } paradl_config;
 
-/* Phase breakdown of one configuration (phases of P:755), per iteration. */
+/* Phase breakdown of one configuration (phases of P:755), per iteration.  SPATIAL_AG
+ * reports its boundary Allgather in t_fb_ag; GPIPE reports the whole schedule time
+ * (compute, boundary sends, WU) in t_comp. */
 typedef struct {
     double t_comp, t_ge, t_fb_ag, t_fb_ar, t_halo, t_p2p, t_iter, t_epoch, mem, I;
     uint32_t reason;

@@ -147,7 +147,7 @@ extern "C" void paradl_destroy(paradl_ctx *c) {
 }
 
 extern "C" const char *paradl_last_error(const paradl_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
-extern "C" const char *paradl_version(void) { return "paradl-b200 1.0 (sm_100a)"; }
+extern "C" const char *paradl_version(void) { return "paradl-b200 1.1 (sm_100a)"; }
 
 extern "C" int32_t paradl_struct_size(int32_t which) {
     switch (which) {
@@ -328,8 +328,8 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         const HostModel &m = c->models[s.model_id];
         const int G = (int)m.rows.size();
         const int fam = s.family;
-        const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD;
-        const bool spatial = fam == PARADL_SPATIAL || fam == PARADL_DS;
+        const bool pipe = fam == PARADL_PIPELINE || fam == PARADL_LAYERPURE || fam == PARADL_PD || fam == PARADL_GPIPE;
+        const bool spatial = fam == PARADL_SPATIAL || fam == PARADL_DS || fam == PARADL_SPATIAL_AG;
         if (s.n_cap < 0 || s.n_flops < 0 || s.n_b < 1 || s.n_S < 0 || s.n_dims < 0 || s.n_Ls < 0 || s.n_alpha < 0 ||
             s.n_beta < 0)
             return fail(c, PARADL_EINVAL, "sub %d: negative list length or empty b list", i);
@@ -361,12 +361,12 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
                 if (d[a] < 1 || d[a] > (1 << 24)) return fail(c, PARADL_EINVAL, "sub %d: dims must be in [1, 2^24]", i);
             bool ok = true;
             switch (fam) {
-            case PARADL_SERIAL: case PARADL_PIPELINE: case PARADL_LAYERPURE:
+            case PARADL_SERIAL: case PARADL_PIPELINE: case PARADL_LAYERPURE: case PARADL_GPIPE:
                 ok = d[0] == 1 && d[1] == 1 && d[2] == 1 && d[3] == 1; break;
             case PARADL_DATA: case PARADL_FILTER: case PARADL_CHANNEL: case PARADL_PD:
                 ok = d[1] == 1 && d[2] == 1 && d[3] == 1; break;
             case PARADL_DF: ok = d[2] == 1 && d[3] == 1; break;
-            case PARADL_SPATIAL: ok = d[0] == 1; break;
+            case PARADL_SPATIAL: case PARADL_SPATIAL_AG: ok = d[0] == 1; break;
             default: break;
             }
             if (!ok) return fail(c, PARADL_EINVAL, "sub %d: dims tuple does not fit the family", i);
@@ -377,6 +377,8 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         std::vector<int32_t> Ll(s.Ls, s.Ls + s.n_Ls);
         if (Ll.empty()) Ll.push_back(0);
         for (int32_t v : Ll) if (v < 0) return fail(c, PARADL_EINVAL, "sub %d: Ls must be >= 0", i);
+        if (fam == PARADL_SPATIAL_AG)
+            for (int32_t v : Ll) if (v < 1) return fail(c, PARADL_EINVAL, "sub %d: spatial_ag needs Ls >= 1", i);
         std::vector<double> al, be;
         if (s.n_alpha) al.assign(s.alpha, s.alpha + (size_t)s.n_alpha * NT);
         else for (int t = 0; t < NT; t++) al.push_back(sy.tiers[t].alpha_s);
@@ -393,12 +395,16 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
             if (s.part_mode != PARADL_PART_NONE) return fail(c, PARADL_EINVAL, "sub %d: partition mode on a non-pipeline family", i);
         } else if (s.part_mode == PARADL_PART_MASK) {
             if (G > 64) return fail(c, PARADL_EINVAL, "sub %d: mask mode needs G <= 64", i);
+            if (fam == PARADL_GPIPE && G > PARADL_GPIPE_MAX_STAGES)
+                return fail(c, PARADL_EINVAL, "sub %d: gpipe mask mode needs G <= %d", i, PARADL_GPIPE_MAX_STAGES);
             part_n = (uint64_t)1 << (G - 1);
             h.s_min = 1;
             h.s_max = G;
         } else if (s.part_mode == PARADL_PART_COMB) {
             if (s.s_min < 1 || s.s_max < s.s_min || s.s_max > G) return fail(c, PARADL_EINVAL, "sub %d: need 1 <= s_min <= s_max <= G", i);
             if (s.s_max - 1 > kMaxCuts) return fail(c, PARADL_EINVAL, "sub %d: combination mode supports s_max <= %d", i, kMaxCuts + 1);
+            if (fam == PARADL_GPIPE && s.s_max > PARADL_GPIPE_MAX_STAGES)
+                return fail(c, PARADL_EINVAL, "sub %d: gpipe supports s_max <= %d", i, PARADL_GPIPE_MAX_STAGES);
             h.s_min = s.s_min;
             h.s_max = s.s_max;
             h.kmax = s.s_max - 1;
@@ -728,7 +734,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 stride_digits(h, w);
             }
         }
-        if (fam == PARADL_SPATIAL || fam == PARADL_DS) {
+        if (fam == PARADL_GPIPE) {
+            // per-lane stage table (f, g, m, u per stage) of the GPipe schedule evaluation
+            a.dtab_bytes = std::max<uint32_t>(a.dtab_bytes, kGpipeTabBytes);
+        }
+        if (fam == PARADL_SPATIAL || fam == PARADL_DS || fam == PARADL_SPATIAL_AG) {
             HaloJob &j = hj.job[hj.n_jobs++];
             j.sub = (int32_t)q;
             j.n_entries = (int32_t)(h.radix[D_DIMS] * h.radix[D_LS]);
@@ -756,6 +766,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     x.memo_bytes = memo_bytes;
                     x.low_bytes = low_bytes;
                     x.dtab_bytes = md == 1 ? dtab_bytes : 0;
+                } else if (fam_of[li] == PARADL_GPIPE) {
+                    x.dtab_bytes = dtab_bytes;   // per-lane stage table
                 }
                 if (first) {
                     L[li] = x;
@@ -787,7 +799,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     size_t total_ctas = 0;
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
-        if (smem + a.memo_bytes + a.low_bytes + a.dtab_bytes > c->smem_optin) a.dtab_bytes = 0;   // unscreened path
+        if (smem + a.memo_bytes + a.low_bytes + a.dtab_bytes > c->smem_optin) {
+            if (fam_of[li] == PARADL_GPIPE)
+                return fail(c, PARADL_ENOMEM, "image + gpipe stage table exceed shared memory");
+            a.dtab_bytes = 0;   // unscreened path
+        }
         smems[li] = smem + a.memo_bytes + a.low_bytes + a.dtab_bytes;
         const uint64_t okey = ((uint64_t)fam_of[li] << 40) | ((uint64_t)dense << 39) | ((uint64_t)blk_of[li] << 36) |
                               (uint64_t)smems[li];

@@ -354,6 +354,8 @@ struct Mid {
     double pp_c, pp_na, pp_s;
     int pp_t;
     bool pp_on;           // pipeline c (alpha + s beta) / layer-pure 2 (na alpha + s beta)
+    double *gp;           // GPIPE: this lane's stage table f[i], g[i], m[i], u[i] at gp[(4i+k)*gps]
+    int gps, gS, gns;     // table stride, segments S, stage count s
     // memoised divisions (same operands -> same IEEE result; recomputed when an operand changes)
     double R_memo, tau_memo;
     int64_t B_memo;
@@ -478,6 +480,67 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.ge2 = make_ar(H, p1, i2d(dW), ddiv(i2d(dW), i2d(p1)), to);  // Allreduce among leaders
         }
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p, 1);
+    } else if (FAM == PARADL_SPATIAL_AG) {
+        // Spatial on rows [0, Ls), Allgather of y_Ls, rows [Ls, G) replicated (Q35):
+        // comp = ((B FB_pre / p) tau + (B FB_suf) tau) + WU tau; GE = AR(p, delta W);
+        // AG = (p-1)(alpha + (B delta |y_Ls| / p) beta); halo as Spatial over the prefix;
+        // mem = gamma (delta (((2B XY_pre)/p + 2B XY_suf) + 2W) + BI)
+        const int32_t split[3] = {dm[1], dm[2], dm[3]};
+        p = (int64_t)dm[1] * dm[2] * dm[3];
+        B = b;
+        const int32_t Ls = at<int32_t>(v.img, S->off_Ls)[L.d[D_LS]];
+        const int Lp = Ls < M->G ? Ls : M->G;
+        const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+        const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+        const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+        const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+        const int64_t FBp = PF[Lp] + PB[Lp], XYp = PX[Lp];
+        m.comp = dadd(dadd(dmul(div_i(B * FBp, p), tau), dmul(i2d(B * (M->FB - FBp)), tau)), dmul(i2d(M->WU), tau));
+        int64_t NS, HV;
+        if (halo) {
+            const HaloEntry &he = halo[L.d[D_DIMS] * S->radix[D_LS] + L.d[D_LS]];
+            NS = he.NS;
+            HV = he.HV;
+            reason |= he.reason;
+        } else {
+            reason |= spatial_terms(v, Ls, split, NS, HV);
+        }
+        const int t = tier_of(H, p);
+        reason |= flag_tier(t);
+        m.h_on = p > 1;
+        m.h_na = i2d(2 * NS);
+        m.h_s = i2d(b * delta * HV);
+        m.h_t = t;
+        m.ge = make_ar(H, p, i2d(dW), ddiv(i2d(dW), i2d(p)), t);
+        m.ag_on = Lp < M->G && p > 1;
+        m.ag_c = i2d(p - 1);
+        m.ag_na = 1.0;
+        m.ag_s = ddiv(i2d(B * delta * Y[Lp - 1]), i2d(p));
+        m.ag_t = t;
+        m.mem = dmul(H->gamma, dmul(i2d(delta), dadd(dadd(dadd(div_i(2 * B * XYp, p), i2d(2 * B * (M->XY - XYp))),
+                                                          i2d(2 * M->W)),
+                                                     i2d(M->BI))));
+    } else if (FAM == PARADL_GPIPE) {
+        // GPipe schedule (Q36): per-stage f = ((b/S) FW_i) tau, g = ((b/S) BW_i) tau,
+        // m = (b/S) delta |y_i| (boundary message, c_i = alpha + m beta), u = WU_i tau, written
+        // to the lane's stage table; the schedule itself runs per (alpha, beta) in gpipe_time()
+        const int ns = L.ns;
+        const int64_t Sg = at<int32_t>(v.img, S->off_S)[L.d[D_S]];
+        p = ns;
+        B = b;
+        const int ts = tier_of(H, ns);
+        reason |= flag_tier(ts);
+        if (b != m.bS_b || Sg != m.bS_S) {
+            m.bS_b = b;
+            m.bS_S = Sg;
+            m.bS_memo = ddiv(i2d(b), i2d(Sg));
+        }
+        m.comp = 0.0;
+        m.pp_t = ts;
+        m.gS = (int)Sg;
+        m.gns = ns;
+        m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
+        if (Sg > b) reason |= PARADL_R_SEGMENTS;
     } else if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL) {   // Filter / Channel rows
         p = dm[0];
         B = b;
@@ -555,6 +618,140 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
     m.p = p;
 }
 
+// GPIPE stage table of the lane (after compute_mid<PARADL_GPIPE>, which set m.bS_memo = b/S
+// and m.tau_memo): per stage i, f = ((b/S) FW_i) tau, g = ((b/S) BW_i) tau, m = (b/S)(delta
+// |y_i|) for i < s-1 (else 0), u = WU_i tau; stage sums by prefix differences (exact int64).
+__device__ void gpipe_fill(const View &v, const Lane &L, const uint16_t *cuts, int cs, Mid &m) {
+    const ModelHdr *M = v.M;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    const int64_t delta = v.H->delta;
+    const double mb = m.bS_memo, tau = m.tau_memo;
+    const bool maskm = v.S->part_mode == PARADL_PART_MASK;
+    uint64_t mask = L.part;
+    int beg = 0;
+    for (int i = 0; i < L.ns; i++) {
+        int end;
+        if (i == L.ns - 1) end = M->G;
+        else if (maskm) {
+            end = __ffsll((long long)mask);   // bit j set <=> cut after row j+1
+            mask &= mask - 1;
+        } else end = cuts[i * cs];
+        double *q = m.gp + (size_t)(4 * i) * m.gps;
+        q[0] = dmul(dmul(mb, i2d(PF[end] - PF[beg])), tau);
+        q[m.gps] = dmul(dmul(mb, i2d(PB[end] - PB[beg])), tau);
+        q[2 * m.gps] = i < L.ns - 1 ? dmul(mb, i2d(delta * Y[end - 1])) : 0.0;
+        q[3 * m.gps] = dmul(i2d(PU[end] - PU[beg]), tau);
+        beg = end;
+    }
+}
+
+// The GPipe schedule (Q36) for NC (alpha, beta) pairs of the stage tier,
+// evaluated as NC interleaved chains (ILP): S segments flow through the NS stages; forward
+// stage i is busy f_i + c_i (blocking send of y_i, c_i = alpha + m_i beta), backward stage i
+// is busy g_i + c_{i-1}; backward starts at the forward makespan; stage i applies WU after its
+// last backward segment.  Each task starts at max(stage free, input delivered) -- the oracle's
+// event simulation, whose additions this performs operand for operand.  The maxima the
+// oracle takes against a value known to be smaller are skipped (max returns an operand
+// exactly): stage 0 forward is ready at 0 <= its free time; segment 0 finds every stage free
+// before its input arrives (free = 0 forward, = t_f <= ready backward); the last stage's
+// backward input is ready at t_f <= its free time.
+template <int NS, int NC>
+__device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const double *a, const double *be,
+                                          double *t) {
+    double dfw[NC][NS], dbw[NC][NS], fr[NC][NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        const double f = q[(4 * i) * gs], g = q[(4 * i + 1) * gs];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            dfw[c][i] = f;
+            dbw[c][i] = g;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i + 1 < NS; i++) {
+        const double mi = q[(4 * i + 2) * gs];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            const double ci = dadd(a[c], dmul(mi, be[c]));
+            dfw[c][i] = dadd(dfw[c][i], ci);
+            dbw[c][i + 1] = dadd(dbw[c][i + 1], ci);
+        }
+    }
+    // forward wave, segment 0 then 1..S-1
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        fr[c][0] = dfw[c][0];
+#pragma unroll
+        for (int i = 1; i < NS; i++) fr[c][i] = dadd(fr[c][i - 1], dfw[c][i]);
+    }
+    for (int j = 1; j < S; j++) {
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            fr[c][0] = dadd(fr[c][0], dfw[c][0]);
+#pragma unroll
+            for (int i = 1; i < NS; i++) fr[c][i] = dadd(fmax(fr[c][i], fr[c][i - 1]), dfw[c][i]);
+        }
+    }
+    // backward wave (GPipe flush at t_f = fr[NS-1]), segment 0 then 1..S-1
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        fr[c][NS - 1] = dadd(fr[c][NS - 1], dbw[c][NS - 1]);
+#pragma unroll
+        for (int i = NS - 2; i >= 0; i--) fr[c][i] = dadd(fr[c][i + 1], dbw[c][i]);
+    }
+    for (int j = 1; j < S; j++) {
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            fr[c][NS - 1] = dadd(fr[c][NS - 1], dbw[c][NS - 1]);
+#pragma unroll
+            for (int i = NS - 2; i >= 0; i--) fr[c][i] = dadd(fmax(fr[c][i], fr[c][i + 1]), dbw[c][i]);
+        }
+    }
+    // weight update after each stage's last backward segment
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        const double u = q[(4 * i + 3) * gs];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            const double e = dadd(fr[c][i], u);
+            t[c] = i == 0 ? e : fmax(t[c], e);   // the oracle's max(0, e_0) = e_0 (e_0 >= 0)
+        }
+    }
+}
+
+#ifndef PARADL_GP_INLINE
+#define PARADL_GP_INLINE 1
+#endif
+#if PARADL_GP_INLINE
+#define PARADL_GP_ATTR __forceinline__
+#else
+#define PARADL_GP_ATTR __noinline__
+#endif
+template <int NC>
+__device__ PARADL_GP_ATTR void gpipe_eval(const double *q, int gs, int ns, int S, const double *a, const double *be,
+                                        double *t) {
+    switch (ns) {
+    case 1: gp_chains<1, NC>(q, gs, S, a, be, t); break;
+    case 2: gp_chains<2, NC>(q, gs, S, a, be, t); break;
+    case 3: gp_chains<3, NC>(q, gs, S, a, be, t); break;
+    case 4: gp_chains<4, NC>(q, gs, S, a, be, t); break;
+    case 5: gp_chains<5, NC>(q, gs, S, a, be, t); break;
+    case 6: gp_chains<6, NC>(q, gs, S, a, be, t); break;
+    case 7: gp_chains<7, NC>(q, gs, S, a, be, t); break;
+    default: gp_chains<kGpMax, NC>(q, gs, S, a, be, t); break;
+    }
+}
+
+__device__ __forceinline__ double gpipe_time(const Mid &m, double a, double be) {
+    double t[1];
+    gpipe_eval<1>(m.gp, m.gps, m.gns, m.gS, &a, &be, t);
+    return t[0];
+}
+
 struct Phases {
     double comp, ge, ag, ar, halo, p2p;
 };
@@ -566,15 +763,28 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
     double ge = 0.0, ag = 0.0, ar = 0.0, halo = 0.0, p2p = 0.0;
     double t = m.comp;
     if (!EXPLAIN && CHECK_TIER && (m.reason & PARADL_R_TIER)) return CUDART_INF;
+    if (FAM == PARADL_GPIPE) {
+        t = (EXPLAIN && m.pp_t < 0) ? CUDART_INF : gpipe_time(m, arow[max(m.pp_t, 0)], brow[max(m.pp_t, 0)]);
+        if (EXPLAIN) {
+            ph->comp = t;
+            ph->ge = ph->ag = ph->ar = ph->halo = ph->p2p = 0.0;
+        }
+        return t;
+    }
     auto ar_eval = [&](const ARt &r, double phi, bool use_phi) -> double {
         if (!r.on) return 0.0;
         if (EXPLAIN && r.t < 0) return CUDART_INF;
         const double bh = use_phi ? dmul(brow[r.t], phi) : brow[r.t];
         return dmul(r.c, dadd(arow[r.t], dmul(r.s, bh)));
     };
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD) {
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_SPATIAL_AG) {
         ge = ar_eval(m.ge, 1.0, false);
         if (m.ge.on) t = dadd(t, ge);
+    }
+    if (FAM == PARADL_SPATIAL_AG && m.ag_on) {   // boundary Allgather
+        if (EXPLAIN && m.ag_t < 0) ag = CUDART_INF;
+        else ag = dmul(m.ag_c, dadd(arow[m.ag_t], dmul(m.ag_s, brow[m.ag_t])));
+        t = dadd(t, ag);
     }
     if (FAM == PARADL_DS) {
         ge = dadd(ar_eval(m.ge, 1.0, false), ar_eval(m.ge2, 1.0, false));
@@ -592,7 +802,7 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
             t = dadd(dadd(t, ag), ar);
         }
     }
-    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) {
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) {
         if (m.h_on) {
             if (EXPLAIN && m.h_t < 0) halo = CUDART_INF;
             else halo = dmul(2.0, dadd(dmul(m.h_na, arow[m.h_t]), dmul(m.h_s, brow[m.h_t])));
@@ -654,37 +864,41 @@ struct SlotV {
 
 template <int FAM>
 __device__ __forceinline__ void alpha_vals(const Mid &m, const double *arow, AlphaV &a) {
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_DF)
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_DF ||
+        FAM == PARADL_SPATIAL_AG)
         a.ge = arow[m.ge.t];
     if (FAM == PARADL_DS) a.ge2 = arow[m.ge2.t];
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) a.ag = dmul(m.ag_na, arow[m.ag_t]);
-    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) a.h = dmul(m.h_na, arow[m.h_t]);
+    if (FAM == PARADL_SPATIAL_AG) a.ag = arow[m.ag_t];
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) a.h = dmul(m.h_na, arow[m.h_t]);
     if (FAM == PARADL_PIPELINE || FAM == PARADL_PD) a.pp = arow[m.pp_t];
     if (FAM == PARADL_LAYERPURE) a.pp = dmul(m.pp_na, arow[m.pp_t]);
 }
 
 template <int FAM>
 __device__ __forceinline__ void slot_vals(const Mid &m, const double *brow, SlotV &v) {
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS)
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG)
         v.ge = dmul(m.ge.s, brow[m.ge.t]);
     if (FAM == PARADL_DF) v.ge = dmul(m.ge.s, dmul(brow[m.ge.t], m.phi));
     if (FAM == PARADL_DS) v.ge2 = dmul(m.ge2.s, brow[m.ge2.t]);
-    if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) v.ag = dmul(m.ag_s, brow[m.ag_t]);
-    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) v.h = dmul(m.h_s, brow[m.h_t]);
+    if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF || FAM == PARADL_SPATIAL_AG)
+        v.ag = dmul(m.ag_s, brow[m.ag_t]);
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) v.h = dmul(m.h_s, brow[m.h_t]);
     if (FAM == PARADL_PIPELINE || FAM == PARADL_PD || FAM == PARADL_LAYERPURE) v.pp = dmul(m.pp_s, brow[m.pp_t]);
 }
 
 template <int FAM>
 __device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const SlotV &v) {
     double t = m.comp;
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DF)
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DF || FAM == PARADL_SPATIAL_AG)
         t = dadd(t, dmul(m.ge.c, dadd(a.ge, v.ge)));
+    if (FAM == PARADL_SPATIAL_AG) t = dadd(t, dmul(m.ag_c, dadd(a.ag, v.ag)));
     if (FAM == PARADL_DS) t = dadd(t, dadd(dmul(m.ge.c, dadd(a.ge, v.ge)), dmul(m.ge2.c, dadd(a.ge2, v.ge2))));
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) {
         const double ag = dmul(m.ag_c, dadd(a.ag, v.ag));
         t = dadd(dadd(t, ag), dmul(2.0, ag));
     }
-    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) t = dadd(t, dmul(2.0, dadd(a.h, v.h)));
+    if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) t = dadd(t, dmul(2.0, dadd(a.h, v.h)));
     if (FAM == PARADL_PIPELINE || FAM == PARADL_PD) t = dadd(t, dmul(m.pp_c, dadd(a.pp, v.pp)));
     if (FAM == PARADL_LAYERPURE) t = dadd(t, dmul(2.0, dadd(a.pp, v.pp)));
     return t;
@@ -692,6 +906,7 @@ __device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const S
 
 template <int FAM>
 __device__ __forceinline__ double inner_fast(const Mid &m, const double *arow, const double *brow) {
+    if constexpr (FAM == PARADL_GPIPE) return gpipe_time(m, arow[m.pp_t], brow[m.pp_t]);
     AlphaV a;
     SlotV v;
     alpha_vals<FAM>(m, arow, a);
@@ -916,7 +1131,8 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
     // the light families, 8 where more comm terms would spill); the admission test is one
     // ballot per key (no min/select sequence)
     constexpr int KEYS = (FAM == PARADL_PIPELINE || FAM == PARADL_DATA || FAM == PARADL_LAYERPURE) ? 16
-                         : (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_DF)        ? 4
+                         : (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_DF ||
+                            FAM == PARADL_SPATIAL_AG)                                             ? 4
                                                                                                   : 8;
     constexpr int R = KEYS / M;
     const double *ap = alpha_tab + (size_t)a * NT;
@@ -1008,7 +1224,7 @@ struct __align__(16) SmemExtra {
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
 template <int FAM, bool DENSE>
 __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
-                                          uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt) {
+                                          uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, double *dtab) {
     const View v = make_view(smem, w.sub);
     const int lane = threadIdx.x & 31;
     const int cs = kThreads;
@@ -1017,13 +1233,14 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
     const double *beta_tab = at<double>(v.img, v.S->off_beta);
     const uint64_t gbase = v.S->offset;   // global index of local index 0
     const uint64_t TS = 32ull * w.steps;
-    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
+    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD || FAM == PARADL_GPIPE;
+    constexpr bool GP = FAM == PARADL_GPIPE;
     const uint32_t nB = v.S->radix[D_BETA];
     const uint32_t nAB = v.S->radix[D_ALPHA] * nB;     // host guarantees < 2^31
     const uint32_t dB = 32u % nB, dA = 32u / nB;        // lane stride 32 inside the alpha/beta block
     // beta-slot caching (M = nB / 32) needs every lane of a step in the same 32-aligned beta
     // window, i.e. a 32-aligned range start (tile starts are lo + multiples of 32)
-    const bool slots = (nB == 32u || nB == 64u) && (w.lo & 31u) == 0;
+    const bool slots = !GP && (nB == 32u || nB == 64u) && (w.lo & 31u) == 0;
     const bool M2 = nB == 64u;
     const unsigned full = 0xffffffffu;
         const uint64_t u0 = w.lo + tile * TS;
@@ -1037,10 +1254,15 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         StageT st;
         Mid m;
         m.reset_memo();
+        if (GP) {
+            m.gp = dtab + threadIdx.x;
+            m.gps = kThreads;
+        }
         if ((uint32_t)lane < len) {
             decode(v, u0 + lane, L, cuts, cs);
             if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
             compute_mid<FAM>(v, L, st, m, w.halo);
+            if (GP) gpipe_fill(v, L, cuts, cs, m);
             fastify(m);
         } else {
             L.d[D_ALPHA] = L.d[D_BETA] = 0;
@@ -1114,8 +1336,50 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 } else if (fb == full && slots) {
                     // every lane feasible and n_beta = 32*M: lane's beta values are fixed, so the
                     // s*beta products are formed once per run and reused for every alpha row
-                    if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
-                    else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                    if constexpr (!GP) {
+                        if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                        else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                    }
+                } else if (GP && fb == full) {
+                    // GPipe schedule: two (alpha, beta) configurations per call, interleaved chains
+                    const int ts = m.pp_t;
+                    uint32_t r = 0;
+                    for (; r + 1 < run; r += 2) {
+                        double av[2], bv[2], kv[2];
+                        av[0] = alpha_tab[(size_t)alpha_i * NT + ts];
+                        bv[0] = beta_tab[(size_t)beta_i * NT + ts];
+                        beta_i += dB;
+                        alpha_i += dA;
+                        if (beta_i >= nB) {
+                            beta_i -= nB;
+                            alpha_i++;
+                        }
+                        av[1] = alpha_tab[(size_t)alpha_i * NT + ts];
+                        bv[1] = beta_tab[(size_t)beta_i * NT + ts];
+                        beta_i += dB;
+                        alpha_i += dA;
+                        if (beta_i >= nB) {
+                            beta_i -= nB;
+                            alpha_i++;
+                        }
+                        gpipe_eval<2>(m.gp, m.gps, m.gns, m.gS, av, bv, kv);
+                        const double k0 = dmul(kv[0], m.I), k1 = dmul(kv[1], m.I);
+                        if (__any_sync(full, k0 <= tk.adm || k1 <= tk.adm)) {
+                            tk.offer(true, k0, g0 + lane + 32ull * (j + r));
+                            tk.offer(true, k1, g0 + lane + 32ull * (j + r + 1));
+                        }
+                    }
+                    if (r < run) {
+                        const double key = dmul(gpipe_time(m, alpha_tab[(size_t)alpha_i * NT + ts],
+                                                           beta_tab[(size_t)beta_i * NT + ts]),
+                                                m.I);
+                        if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
+                    }
+                    {
+                        const uint32_t nab = ab + 32u * (run - 1);
+                        alpha_i = nab / nB;
+                        beta_i = nab - alpha_i * nB;
+                    }
                 } else if (fb == full) {
                     // every lane feasible: branch-free evaluation, rare slow path for insertions
 #pragma unroll 2
@@ -1183,6 +1447,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     if (PIPE && lvl >= D_PART)
                         stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
                     compute_mid<FAM>(v, L, st, m, w.halo);
+                    if (GP) gpipe_fill(v, L, cuts, cs, m);
                     fastify(m);
                 }
                 alpha_i = L.d[D_ALPHA];
@@ -1929,8 +2194,11 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
     __syncthreads();
 }
 
+#ifndef PARADL_MINB
+#define PARADL_MINB 2
+#endif
 template <int FAM, bool DENSE, int BLK>
-__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1 : PARADL_MINB) sweep_kernel(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ unsigned long long s_count;
@@ -1969,7 +2237,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
         }
         else
-            tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt);
+            tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt, dtab);
     }
 
     if (!DENSE) {
@@ -2116,11 +2384,15 @@ __device__ void explain_one(const View &v, const Lane &L, const uint16_t *cuts, 
                             paradl_prediction *pr) {
     StageT st = {};
     const int64_t b = at<int64_t>(v.img, v.S->off_b)[L.d[D_B]];
-    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD;
+    constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD || FAM == PARADL_GPIPE;
     if (PIPE) stage_terms(v, L, cuts, 1, b, st);
     Mid m;
     m.reset_memo();
+    double gtab[4 * kGpMax];
+    m.gp = gtab;
+    m.gps = 1;
     compute_mid<FAM>(v, L, st, m);
+    if (FAM == PARADL_GPIPE) gpipe_fill(v, L, cuts, 1, m);
     const int NT = v.H->n_tiers;
     const double *arow = at<double>(v.img, v.S->off_alpha) + (size_t)L.d[D_ALPHA] * NT;
     const double *brow = at<double>(v.img, v.S->off_beta) + (size_t)L.d[D_BETA] * NT;
@@ -2199,6 +2471,8 @@ __global__ void explain_kernel(const uint8_t *img, int32_t sub, uint64_t local, 
     case PARADL_PIPELINE: explain_one<PARADL_PIPELINE>(v, L, cuts, cfg, pr); break;
     case PARADL_LAYERPURE: explain_one<PARADL_LAYERPURE>(v, L, cuts, cfg, pr); break;
     case PARADL_PD: explain_one<PARADL_PD>(v, L, cuts, cfg, pr); break;
+    case PARADL_SPATIAL_AG: explain_one<PARADL_SPATIAL_AG>(v, L, cuts, cfg, pr); break;
+    case PARADL_GPIPE: explain_one<PARADL_GPIPE>(v, L, cuts, cfg, pr); break;
     default: break;
     }
 }
@@ -2395,6 +2669,8 @@ static void *sweep_fn(int family, bool dense, int blk) {
         PARADL_CASE(PARADL_PIPELINE)
         PARADL_CASE(PARADL_LAYERPURE)
         PARADL_CASE(PARADL_PD)
+        PARADL_CASE(PARADL_SPATIAL_AG)
+        PARADL_CASE(PARADL_GPIPE)
     default: return nullptr;
     }
 #undef PARADL_CASE

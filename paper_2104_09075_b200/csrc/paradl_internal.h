@@ -26,6 +26,9 @@ constexpr uint32_t kWorkMaskD = 1u;
 constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the screened mask path (n <= 64)
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
+constexpr int kGpMax = PARADL_GPIPE_MAX_STAGES;
+// GPIPE per-lane stage table in shared memory: 4 doubles (f, g, m, u) per stage, column per thread
+constexpr uint32_t kGpipeTabBytes = 4u * kGpMax * 8u * kThreads;
 
 // digits of the canonical mixed radix, fast -> slow
 enum { D_BETA = 0, D_ALPHA, D_LS, D_DIMS, D_S, D_PART, D_B, D_FLOPS, D_CAP, kDigits };

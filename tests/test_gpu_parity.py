@@ -381,3 +381,76 @@ def test_merge_records_equals_single(dev):
         got = [int(v) for v in out.cpu().numpy()[:, 0].astype(np.uint64)]
         assert got == [h[0] for h in single]
         assert int(cnt.item()) == nf
+
+
+# ------------------------------------------------------------------ SURVEY §8(f) next rows
+@pytest.mark.parametrize("name,kw", [("gpipe", dict(n_alpha=3, n_beta=4, b_list=[1, 6, 64], s_max=3)),
+                                     ("gpipe", dict(n_alpha=2, n_beta=32, b_list=[8], s_max=2, S_list=(1, 3, 8))),
+                                     ("spatial_ag", dict(n_alpha=3, n_beta=2))])
+def test_next_rows_reduced(dev, oracle_mod, name, kw):
+    """GPipe schedule family and spatial prefix + Allgather family on reduced sweeps: whole
+    range dense + top-64 against the oracle, then random windows (ragged tails)."""
+    sw = W.NEXT[name](**kw)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    assert ctx.sweep_size(spec) == n
+    if n <= 3_000_000:
+        assert check_dense(ctx, spec, osw, 0, n, dev) == 0
+        check_topk(ctx, spec, osw, 0, n, 64)
+    rng = random.Random(7)
+    for _ in range(5):
+        a = rng.randrange(max(1, n - 50_000))
+        c = min(n - a, rng.randrange(1, 50_000))
+        assert check_dense(ctx, spec, osw, a, c, dev) == 0
+        check_topk(ctx, spec, osw, a, c, 16)
+
+
+@pytest.mark.parametrize("name", ["gpipe", "spatial_ag"])
+def test_next_rows_full_size(dev, oracle_mod, name):
+    """Full-size next-row sweeps (the bench's launch configuration): dense windows and
+    window top-k against the oracle; whole-sweep top-k hits re-evaluated one by one."""
+    sw = W.NEXT[name]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    rng = random.Random(200)
+    for a in [0, n - 3000] + [rng.randrange(n - 3000) for _ in range(8)]:
+        c = rng.randrange(500, 3000)
+        assert check_dense(ctx, spec, osw, a, c, dev) == 0
+        check_topk(ctx, spec, osw, a, c, 8)
+    hits, nf = ctx.topk(spec, 64, 0, n)
+    keys = [h[1] for h in hits]
+    assert keys == sorted(keys) and nf > 0
+    idx = np.array([h[0] for h in hits], np.uint64)
+    _, _, r, key = osw.eval_many(idx)
+    assert np.all(r == 0)
+    assert rel_err(key, keys).max() == 0.0
+
+
+def test_gpipe_schedule_matches_table2_for_equal_stages(dev, oracle_mod):
+    """On the GPU: a model of equal rows split into equal stages gives the Table 2 Layer
+    row's time (PIPELINE family) to rounding, and never more than it otherwise."""
+    from workloads import models as M
+    rows = [M.Layer("eq", M.CONV, 2, 8, 8, (4, 4, 1), (4, 4, 1), (3, 3, 1), 128, 128, 576, 8,
+                    100000, 200000, 1152, M.FLAG_COMM) for _ in range(8)]
+    m = M.Model("eq", rows, 1000, default_Ls=8)
+    sysm = W.two_tier_system(flops_per_s=1e12)
+    A, B = W.ab_grid(np.logspace(-7, -4, 8), 1.0 / np.logspace(9, 12, 8))
+    common = dict(part_mode=W.PART_COMB, s_min=1, s_max=8, S=[1, 2, 4, 8], b=[8, 16], alpha=A, beta=B)
+    sw = W.Sweep([m], sysm, [W.SubSweep(W.GPIPE, **common), W.SubSweep(W.PIPELINE, **common)], "eq")
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size() // 2
+    tg, _, _, _ = gpu_dense(ctx, spec, 0, n, dev)
+    tp, _, _, _ = gpu_dense(ctx, spec, n, n, dev)
+    assert np.all(tg <= tp * (1 + 1e-14))
+    for idx in range(0, n, 97):
+        c = osw.decode(idx)
+        ends = list(c.stage_end[:c.n_stages])
+        sizes = np.diff([0] + ends)
+        if np.all(sizes == sizes[0]):
+            assert rel_err([tg[idx]], [tp[idx]]).max() <= 1e-14

@@ -193,3 +193,35 @@ def config5(s_max=6) -> Sweep:
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+
+
+# ----------------------------------------------------------------- SURVEY §8(f) "next" rows
+def next_gpipe(n_alpha=64, n_beta=64, b_list=None, s_max=4, S_list=(1, 2, 4, 8)) -> Sweep:
+    """ResNet-50 partitions timed by the GPipe schedule (family GPIPE, Q36): the
+    shape of config 2's pipeline sub-sweep (s <= 4 exhaustive, S, b, 64x64 alpha/beta)."""
+    m = M.resnet(50)
+    sys = two_tier_system(flops_per_s=37e12, hbm_bytes=16 * GiB)
+    A, B = ab_grid(np.logspace(-7, -4, n_alpha), 1.0 / np.logspace(9, 12, n_beta))
+    b = list(b_list) if b_list is not None else pow2(0, 8)
+    subs = [SubSweep(GPIPE, part_mode=PART_COMB, s_min=1, s_max=s_max, S=list(S_list), b=b, alpha=A, beta=B)]
+    return Sweep([m], sys, subs, "next_gpipe_resnet50")
+
+
+def next_spatial_ag(n_alpha=32, n_beta=32) -> Sweep:
+    """Spatial prefix + Allgather (family SPATIAL_AG, Q35): ResNet-50 2D
+    splits with prefixes ending at each stage boundary, CosmoFlow 128^3 / 512^3 3D splits
+    with the config 4 prefixes, capacities and batches."""
+    r50 = M.resnet(50)
+    ms = [r50, M.cosmoflow(128), M.cosmoflow(512)]
+    sys = two_tier_system(flops_per_s=37e12, hbm_bytes=16 * GiB)
+    A, B = ab_grid(np.logspace(-7, -4, n_alpha), 1.0 / np.logspace(9, 12, n_beta))
+    caps = [16 * GiB, 32 * GiB, 80 * GiB, 180 * GiB]
+    subs = [SubSweep(SPATIAL_AG, model=0, dims=splits_pow2(10, 2, False), b=pow2(0, 8),
+                     Ls=[1, 10, 22, 40, r50.default_Ls], alpha=A, beta=B)]
+    for mi in (1, 2):
+        subs.append(SubSweep(SPATIAL_AG, model=mi, cap=caps, b=[1, 2, 4], dims=splits_pow2(10, 3, False),
+                             Ls=[3, 6, 9, 12, 15], alpha=A, beta=B))
+    return Sweep(ms, sys, subs, "next_spatial_ag")
+
+
+NEXT = {"gpipe": next_gpipe, "spatial_ag": next_spatial_ag}
