@@ -658,6 +658,15 @@ __device__ void gpipe_fill(const View &v, const Lane &L, const uint16_t *cuts, i
 // exactly): stage 0 forward is ready at 0 <= its free time; segment 0 finds every stage free
 // before its input arrives (free = 0 forward, = t_f <= ready backward); the last stage's
 // backward input is ready at t_f <= its free time.
+#ifndef PARADL_GP_QUAD
+#define PARADL_GP_QUAD 2
+#endif
+constexpr uint32_t kGpQuad = PARADL_GP_QUAD;   // GPipe configurations per schedule call
+
+// max of two non-negative, non-NaN doubles as one compare + two 32-bit selects (fmax adds
+// NaN handling: a third ALU instruction per max on sm_100a, which has no DMNMX)
+__device__ __forceinline__ double dmax_nn(double a, double b) { return a > b ? a : b; }
+
 template <int NS, int NC>
 __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const double *a, const double *be,
                                           double *t) {
@@ -693,7 +702,7 @@ __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const 
         for (int c = 0; c < NC; c++) {
             fr[c][0] = dadd(fr[c][0], dfw[c][0]);
 #pragma unroll
-            for (int i = 1; i < NS; i++) fr[c][i] = dadd(fmax(fr[c][i], fr[c][i - 1]), dfw[c][i]);
+            for (int i = 1; i < NS; i++) fr[c][i] = dadd(dmax_nn(fr[c][i], fr[c][i - 1]), dfw[c][i]);
         }
     }
     // backward wave (GPipe flush at t_f = fr[NS-1]), segment 0 then 1..S-1
@@ -708,7 +717,7 @@ __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const 
         for (int c = 0; c < NC; c++) {
             fr[c][NS - 1] = dadd(fr[c][NS - 1], dbw[c][NS - 1]);
 #pragma unroll
-            for (int i = NS - 2; i >= 0; i--) fr[c][i] = dadd(fmax(fr[c][i], fr[c][i + 1]), dbw[c][i]);
+            for (int i = NS - 2; i >= 0; i--) fr[c][i] = dadd(dmax_nn(fr[c][i], fr[c][i + 1]), dbw[c][i]);
         }
     }
     // weight update after each stage's last backward segment
@@ -718,7 +727,7 @@ __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const 
 #pragma unroll
         for (int c = 0; c < NC; c++) {
             const double e = dadd(fr[c][i], u);
-            t[c] = i == 0 ? e : fmax(t[c], e);   // the oracle's max(0, e_0) = e_0 (e_0 >= 0)
+            t[c] = i == 0 ? e : dmax_nn(t[c], e);   // the oracle's max(0, e_0) = e_0 (e_0 >= 0)
         }
     }
 }
@@ -731,18 +740,28 @@ __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const 
 #else
 #define PARADL_GP_ATTR __noinline__
 #endif
+// NC configurations at once: up to 4 stages as NC interleaved chains; beyond that (more
+// registers per chain) as NC/2-wide halves
 template <int NC>
 __device__ PARADL_GP_ATTR void gpipe_eval(const double *q, int gs, int ns, int S, const double *a, const double *be,
                                         double *t) {
+    constexpr int H = NC > 2 ? 2 : NC;
     switch (ns) {
     case 1: gp_chains<1, NC>(q, gs, S, a, be, t); break;
     case 2: gp_chains<2, NC>(q, gs, S, a, be, t); break;
     case 3: gp_chains<3, NC>(q, gs, S, a, be, t); break;
     case 4: gp_chains<4, NC>(q, gs, S, a, be, t); break;
-    case 5: gp_chains<5, NC>(q, gs, S, a, be, t); break;
-    case 6: gp_chains<6, NC>(q, gs, S, a, be, t); break;
-    case 7: gp_chains<7, NC>(q, gs, S, a, be, t); break;
-    default: gp_chains<kGpMax, NC>(q, gs, S, a, be, t); break;
+    default:
+#pragma unroll 1
+        for (int h = 0; h < NC; h += H) {
+            switch (ns) {
+            case 5: gp_chains<5, H>(q, gs, S, a + h, be + h, t + h); break;
+            case 6: gp_chains<6, H>(q, gs, S, a + h, be + h, t + h); break;
+            case 7: gp_chains<7, H>(q, gs, S, a + h, be + h, t + h); break;
+            default: gp_chains<kGpMax, H>(q, gs, S, a + h, be + h, t + h); break;
+            }
+        }
+        break;
     }
 }
 
@@ -1343,37 +1362,45 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 } else if (GP && fb == full) {
                     // GPipe schedule: two (alpha, beta) configurations per call, interleaved chains
                     const int ts = m.pp_t;
+                    constexpr uint32_t Q = kGpQuad;
                     uint32_t r = 0;
-                    for (; r + 1 < run; r += 2) {
-                        double av[2], bv[2], kv[2];
-                        av[0] = alpha_tab[(size_t)alpha_i * NT + ts];
-                        bv[0] = beta_tab[(size_t)beta_i * NT + ts];
-                        beta_i += dB;
-                        alpha_i += dA;
-                        if (beta_i >= nB) {
-                            beta_i -= nB;
-                            alpha_i++;
+                    for (; r + Q <= run; r += Q) {
+                        double av[Q], bv[Q], kv[Q];
+#pragma unroll
+                        for (uint32_t c = 0; c < Q; c++) {
+                            av[c] = alpha_tab[(size_t)alpha_i * NT + ts];
+                            bv[c] = beta_tab[(size_t)beta_i * NT + ts];
+                            beta_i += dB;
+                            alpha_i += dA;
+                            if (beta_i >= nB) {
+                                beta_i -= nB;
+                                alpha_i++;
+                            }
                         }
-                        av[1] = alpha_tab[(size_t)alpha_i * NT + ts];
-                        bv[1] = beta_tab[(size_t)beta_i * NT + ts];
-                        beta_i += dB;
-                        alpha_i += dA;
-                        if (beta_i >= nB) {
-                            beta_i -= nB;
-                            alpha_i++;
+                        gpipe_eval<Q>(m.gp, m.gps, m.gns, m.gS, av, bv, kv);
+                        bool any = false;
+#pragma unroll
+                        for (uint32_t c = 0; c < Q; c++) {
+                            kv[c] = dmul(kv[c], m.I);
+                            any |= kv[c] <= tk.adm;
                         }
-                        gpipe_eval<2>(m.gp, m.gps, m.gns, m.gS, av, bv, kv);
-                        const double k0 = dmul(kv[0], m.I), k1 = dmul(kv[1], m.I);
-                        if (__any_sync(full, k0 <= tk.adm || k1 <= tk.adm)) {
-                            tk.offer(true, k0, g0 + lane + 32ull * (j + r));
-                            tk.offer(true, k1, g0 + lane + 32ull * (j + r + 1));
+                        if (__any_sync(full, any)) {
+#pragma unroll
+                            for (uint32_t c = 0; c < Q; c++) tk.offer(true, kv[c], g0 + lane + 32ull * (j + r + c));
                         }
                     }
-                    if (r < run) {
+#pragma unroll 1
+                    for (; r < run; r++) {
                         const double key = dmul(gpipe_time(m, alpha_tab[(size_t)alpha_i * NT + ts],
                                                            beta_tab[(size_t)beta_i * NT + ts]),
                                                 m.I);
                         if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
+                        beta_i += dB;
+                        alpha_i += dA;
+                        if (beta_i >= nB) {
+                            beta_i -= nB;
+                            alpha_i++;
+                        }
                     }
                     {
                         const uint32_t nab = ab + 32u * (run - 1);

@@ -207,7 +207,7 @@ def next_gpipe(n_alpha=64, n_beta=64, b_list=None, s_max=4, S_list=(1, 2, 4, 8))
     return Sweep([m], sys, subs, "next_gpipe_resnet50")
 
 
-def next_spatial_ag(n_alpha=32, n_beta=32) -> Sweep:
+def next_spatial_ag(n_alpha=64, n_beta=64) -> Sweep:
     """Spatial prefix + Allgather (family SPATIAL_AG, Q35): ResNet-50 2D
     splits with prefixes ending at each stage boundary, CosmoFlow 128^3 / 512^3 3D splits
     with the config 4 prefixes, capacities and batches."""
