@@ -371,9 +371,19 @@ struct Mid {
 
 // comp row of Table 2: ((B FB)/p_c) tau + (WU/p_u) tau
 // x / 1.0 == x exactly, so a division by 1 is skipped
+// and x / 2^k is x * 2^-k exactly (integer numerators: the quotient is 0 or >= 2^-62, never
+// subnormal), so only a non-power-of-two divisor pays a true IEEE division
 __device__ __forceinline__ double div_i(int64_t num, int64_t den) {
-    return den == 1 ? i2d(num) : ddiv(i2d(num), i2d(den));
+    if (den == 1) return i2d(num);
+    if ((den & (den - 1)) == 0) {
+        const int k = 63 - __clzll(den);
+        return dmul(i2d(num), __hiloint2double((1023 - k) << 20, 0));
+    }
+    return ddiv(i2d(num), i2d(den));
 }
+// a division taken only when a memoised operand changes: out of line, so the compiler
+// cannot if-convert it into every call
+__device__ __noinline__ double ddiv_rare(double a, double b) { return ddiv(a, b); }
 __device__ __forceinline__ double comp_term(int64_t BFB, int64_t WU, int64_t pc, int64_t pu, double tau) {
     return dadd(dmul(div_i(BFB, pc), tau), dmul(div_i(WU, pu), tau));
 }
@@ -427,7 +437,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
     const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
     if (R != m.R_memo) {
         m.R_memo = R;
-        m.tau_memo = ddiv(1.0, R);
+        m.tau_memo = ddiv_rare(1.0, R);
     }
     const double tau = m.tau_memo;
     const int64_t b = at<int64_t>(v.img, S->off_b)[L.d[D_B]];
@@ -447,7 +457,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.comp = comp_term(B * M->FB, M->WU, p, 1, tau);
         const int t = tier_of(H, p);
         reason |= flag_tier(t);
-        m.ge = make_ar(H, p, i2d(dW), ddiv(i2d(dW), i2d(p)), t);
+        m.ge = make_ar(H, p, i2d(dW), div_i(dW, p), t);
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p, 1);
         if (p > B) reason |= PARADL_R_SCALING;
     } else if (FAM == PARADL_SPATIAL || FAM == PARADL_DS) {   // Spatial row; ds (Q16)
@@ -474,10 +484,10 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.h_s = i2d(b * delta * HV);
         m.h_t = ti;
         if (FAM == PARADL_SPATIAL) {
-            m.ge = make_ar(H, p, i2d(dW), ddiv(i2d(dW), i2d(p)), to);
+            m.ge = make_ar(H, p, i2d(dW), div_i(dW, p), to);
         } else {
-            m.ge = make_ar(H, p2, i2d(dW), ddiv(i2d(dW), i2d(p2)), ti);   // reduce to leader
-            m.ge2 = make_ar(H, p1, i2d(dW), ddiv(i2d(dW), i2d(p1)), to);  // Allreduce among leaders
+            m.ge = make_ar(H, p2, i2d(dW), div_i(dW, p2), ti);   // reduce to leader
+            m.ge2 = make_ar(H, p1, i2d(dW), div_i(dW, p1), to);  // Allreduce among leaders
         }
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p, 1);
     } else if (FAM == PARADL_SPATIAL_AG) {
@@ -511,11 +521,11 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.h_na = i2d(2 * NS);
         m.h_s = i2d(b * delta * HV);
         m.h_t = t;
-        m.ge = make_ar(H, p, i2d(dW), ddiv(i2d(dW), i2d(p)), t);
+        m.ge = make_ar(H, p, i2d(dW), div_i(dW, p), t);
         m.ag_on = Lp < M->G && p > 1;
         m.ag_c = i2d(p - 1);
         m.ag_na = 1.0;
-        m.ag_s = ddiv(i2d(B * delta * Y[Lp - 1]), i2d(p));
+        m.ag_s = div_i(B * delta * Y[Lp - 1], p);
         m.ag_t = t;
         m.mem = dmul(H->gamma, dmul(i2d(delta), dadd(dadd(dadd(div_i(2 * B * XYp, p), i2d(2 * B * (M->XY - XYp))),
                                                           i2d(2 * M->W)),
@@ -533,7 +543,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         if (b != m.bS_b || Sg != m.bS_S) {
             m.bS_b = b;
             m.bS_S = Sg;
-            m.bS_memo = ddiv(i2d(b), i2d(Sg));
+            m.bS_memo = div_i(b, Sg);
         }
         m.comp = 0.0;
         m.pp_t = ts;
@@ -550,7 +560,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.ag_on = p > 1;
         m.ag_c = i2d(p - 1);
         m.ag_na = i2d(M->NC);
-        m.ag_s = ddiv(i2d(B * delta * M->YC), i2d(p));
+        m.ag_s = div_i(B * delta * M->YC, p);
         m.ag_t = t;
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, 1, p);
         if (FAM == PARADL_FILTER ? (p > M->Fmin) : (p > M->Cmin2)) reason |= PARADL_R_SCALING;
@@ -564,10 +574,10 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.ag_on = p2 > 1;
         m.ag_c = i2d(p2 - 1);
         m.ag_na = i2d(M->NC);
-        m.ag_s = ddiv(i2d(B * delta * M->YC), i2d(p));
+        m.ag_s = div_i(B * delta * M->YC, p);
         m.ag_t = ti;
         m.phi = p2 > 1 ? H->phi_df : 1.0;
-        m.ge = make_ar(H, p1, ddiv(i2d(dW), i2d(p2)), ddiv(i2d(dW), i2d(p)), to);
+        m.ge = make_ar(H, p1, div_i(dW, p2), div_i(dW, p), to);
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p1, p2);
         if (p2 > M->Fmin) reason |= PARADL_R_SCALING;
     } else {   // PIPELINE, LAYERPURE, PD (Q17)
@@ -588,7 +598,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             if (b != m.bS_b || Sg != m.bS_S) {
                 m.bS_b = b;
                 m.bS_S = Sg;
-                m.bS_memo = ddiv(i2d(b), i2d(Sg));
+                m.bS_memo = div_i(b, Sg);
             }
             const double bS = m.bS_memo;
             const double cseg = dmul(i2d(ns + Sg - 1), bS);
@@ -601,7 +611,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
                 const int tp = tier_of(H, p);
                 reason |= flag_tier(tp);
                 const double mW = i2d(delta * st.maxW);
-                m.ge = make_ar(H, pd, mW, ddiv(mW, i2d(pd)), tp);
+                m.ge = make_ar(H, pd, mW, div_i(delta * st.maxW, pd), tp);
             }
         }
         m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
@@ -609,7 +619,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
     }
     if (B != m.B_memo) {
         m.B_memo = B;
-        m.I_memo = ddiv(i2d(M->D), i2d(B));   // Table 1: I = D/B
+        m.I_memo = div_i(M->D, B);   // Table 1: I = D/B
     }
     m.I = m.I_memo;
     if (!(m.mem <= cap)) reason |= PARADL_R_MEMORY;
@@ -666,6 +676,7 @@ constexpr uint32_t kGpQuad = PARADL_GP_QUAD;   // GPipe configurations per sched
 // max of two non-negative, non-NaN doubles as one compare + two 32-bit selects (fmax adds
 // NaN handling: a third ALU instruction per max on sm_100a, which has no DMNMX)
 __device__ __forceinline__ double dmax_nn(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double dmin_nn(double a, double b) { return a < b ? a : b; }
 
 template <int NS, int NC>
 __device__ __forceinline__ void gp_chains(const double *q, int gs, int S, const double *a, const double *be,
@@ -967,7 +978,7 @@ struct WarpTopK {
         unsigned long long g = gnext;
         if (adm == CUDART_INF) g = *(volatile unsigned long long *)gbound;
         gnext = *(volatile unsigned long long *)gbound;
-        if (g != ~0ull) adm = fmin(adm, fmin(thk, __longlong_as_double((long long)g)));
+        if (g != ~0ull) adm = dmin_nn(adm, dmin_nn(thk, __longlong_as_double((long long)g)));
     }
     // after thk changed: tighten adm and publish a full list's threshold
     __device__ __forceinline__ void publish() {

@@ -454,3 +454,25 @@ def test_gpipe_schedule_matches_table2_for_equal_stages(dev, oracle_mod):
         sizes = np.diff([0] + ends)
         if np.all(sizes == sizes[0]):
             assert rel_err([tg[idx]], [tp[idx]]).max() <= 1e-14
+
+
+@pytest.mark.parametrize("kw", [dict(n_alpha=4, n_beta=8, b_list=[1, 3, 16, 256], pipe_smax=3),
+                                dict(n_alpha=5, n_beta=7, b_list=[2, 64], pipe_smax=3, S_list=(1, 3, 8)),
+                                dict(n_alpha=9, n_beta=64, b_list=[4], pipe_smax=2)])
+def test_pipeline_ab_blocks(dev, oracle_mod, kw):
+    """cfg2-shaped pipeline sub-sweeps (alpha x beta blocks of 32, 35 and 576 configurations,
+    beta-slot reuse when n_beta = 32 M): top-k + count of the whole sub-sweep and of ragged
+    windows against the oracle."""
+    sw = W.config2(**kw)
+    sw.subs = [s for s in sw.subs if s.family == W.PIPELINE]
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    check_topk(ctx, spec, osw, 0, n, 64)
+    check_topk(ctx, spec, osw, 0, n, 1)
+    rng = random.Random(len(kw))
+    for _ in range(4):
+        a = rng.randrange(n // 2)
+        c = rng.randrange(n // 4, n - a)
+        check_topk(ctx, spec, osw, a, c, 32)
