@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,7 +63,7 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one, halo;
+    DevBuf img, lists, counters, results, one, halo, stab;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
     std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
@@ -302,6 +303,16 @@ uint64_t binom_u64(int64_t n, int64_t k) {
 }
 
 }  // namespace
+
+// A/B switch for experiments: PARADL_NO_STRUCT_TABLE=1 recomputes pipeline structure terms
+// inside the sweep kernel instead of reading the structure table (same results)
+static bool struct_table_off() {
+    static const bool off = [] {
+        const char *e = getenv("PARADL_NO_STRUCT_TABLE");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
 
 static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *spec, Plan &P) {
     if (!spec || spec->n_sub < 1 || !spec->sub) return fail(c, PARADL_EINVAL, "empty sweep spec");
@@ -793,6 +804,40 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 for (int j = 0; j < hj.n_jobs; j++)
                     if (hj.job[j].sub == a.work[i].sub) a.work[i].halo = hj.job[j].tab;
     }
+    // pipeline structure tables (reduce mode, lane-strided work items of >= 2^22 configs):
+    // one record per structure, computed by a thread-per-structure kernel before the sweep
+    std::vector<StructJob> sjobs;
+    if (!dense && !struct_table_off()) {
+        uint64_t n_rec = 0;
+        for (auto &a : L)
+            for (int i = 0; i < a.n_work; i++) {
+                WorkItem &w = a.work[i];
+                if (w.mode != 0 || w.family != PARADL_PIPELINE || w.hi - w.lo < (1ull << 22)) continue;
+                const SubHdr &h = P.subs[w.sub].hdr;
+                const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
+                StructJob j{};
+                j.sub = w.sub;
+                j.s_lo = w.lo / nAB;
+                j.n = (w.hi + nAB - 1) / nAB - j.s_lo;
+                w.stab_lo = j.s_lo;
+                w.stab = reinterpret_cast<const PipeRec *>((uintptr_t)n_rec);   // offset until allocated
+                n_rec += j.n;
+                sjobs.push_back(j);
+            }
+        if (n_rec) {
+            CUDA_TRY(c, c->stab.ensure(sizeof(PipeRec) * n_rec));
+            PipeRec *base = (PipeRec *)c->stab.p;
+            size_t q = 0;
+            for (auto &a : L)
+                for (int i = 0; i < a.n_work; i++) {
+                    WorkItem &w = a.work[i];
+                    if (w.mode != 0 || w.family != PARADL_PIPELINE || w.hi - w.lo < (1ull << 22)) continue;
+                    const uint64_t off = (uint64_t)(uintptr_t)w.stab;
+                    w.stab = base + off;
+                    sjobs[q++].out = base + off;
+                }
+        }
+    }
     // tiles and grids
     std::vector<int> grids(nl);
     std::vector<size_t> smems(nl);
@@ -858,6 +903,10 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
 
     if (halo_entries) {
         CUDA_TRY(c, launch_halo_tables(hj, st));
+        c->stat_launches++;
+    }
+    for (const StructJob &j : sjobs) {
+        CUDA_TRY(c, launch_struct_table((const uint8_t *)c->img.p, j, st));
         c->stat_launches++;
     }
     // fork onto internal streams

@@ -1251,6 +1251,31 @@ struct __align__(16) SmemExtra {
     int8_t tier_by_n[PARADL_MAX_STAGES + 8];   // tier_of(n), n <= 64 (mask stage counts)
 };
 
+// Structure terms of the lane's current structure from the pipeline structure table: the
+// structure index is the mixed-radix value of the digits slower than alpha.
+__device__ __forceinline__ uint64_t struct_index(const View &v, const Lane &L) {
+    const SubHdr *S = v.S;
+    uint64_t s = L.d[D_CAP];
+    s = s * S->radix[D_FLOPS] + L.d[D_FLOPS];
+    s = s * S->radix[D_B] + L.d[D_B];
+    s = s * S->part_n + L.part;
+    s = s * S->radix[D_S] + L.d[D_S];
+    s = s * S->radix[D_DIMS] + L.d[D_DIMS];
+    s = s * S->radix[D_LS] + L.d[D_LS];
+    return s;
+}
+__device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) {
+    const PipeRec *r = w.stab + (s - w.stab_lo);
+    const double4 q = *reinterpret_cast<const double4 *>(r);
+    const int2 t = *reinterpret_cast<const int2 *>(&r->reason);
+    m.comp = q.x;
+    m.pp_c = q.y;
+    m.pp_s = q.z;
+    m.I = q.w;
+    m.reason = (uint32_t)t.x;
+    m.pp_t = t.y;
+}
+
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
 template <int FAM, bool DENSE>
 __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
@@ -1265,8 +1290,10 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
     const uint64_t TS = 32ull * w.steps;
     constexpr bool PIPE = FAM == PARADL_PIPELINE || FAM == PARADL_LAYERPURE || FAM == PARADL_PD || FAM == PARADL_GPIPE;
     constexpr bool GP = FAM == PARADL_GPIPE;
+    constexpr bool REC = FAM == PARADL_PIPELINE && !DENSE;
     const uint32_t nB = v.S->radix[D_BETA];
-    const uint32_t nAB = v.S->radix[D_ALPHA] * nB;     // host guarantees < 2^31
+    const uint32_t nA = v.S->radix[D_ALPHA];
+    const uint32_t nAB = nA * nB;                       // host guarantees < 2^31
     const uint32_t dB = 32u % nB, dA = 32u / nB;        // lane stride 32 inside the alpha/beta block
     // beta-slot caching (M = nB / 32) needs every lane of a step in the same 32-aligned beta
     // window, i.e. a 32-aligned range start (tile starts are lo + multiples of 32)
@@ -1288,12 +1315,20 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
             m.gp = dtab + threadIdx.x;
             m.gps = kThreads;
         }
+        // pipeline reduce tiles read the structure terms from the structure table
+        const bool rec = REC && w.stab != nullptr;
+        uint64_t sidx = 0;   // rec: the lane's structure index
         if ((uint32_t)lane < len) {
             decode(v, u0 + lane, L, cuts, cs);
-            if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
-            compute_mid<FAM>(v, L, st, m, w.halo);
-            if (GP) gpipe_fill(v, L, cuts, cs, m);
-            fastify(m);
+            if (rec) {
+                sidx = struct_index(v, L);
+                load_rec(w, sidx, m);
+            } else {
+                if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+                compute_mid<FAM>(v, L, st, m, w.halo);
+                if (GP) gpipe_fill(v, L, cuts, cs, m);
+                fastify(m);
+            }
         } else {
             L.d[D_ALPHA] = L.d[D_BETA] = 0;
             m.reason = PARADL_R_SCALING;
@@ -1476,17 +1511,36 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 }
             }
             j += run;
-            if (j < nsteps && (uint32_t)lane + 32u * j < len) {
+            if (rec && nAB >= 32u && j < nsteps && (uint32_t)lane + 32u * j < len) {
+                // step into the next configuration (32 ahead): with a block of >= 32 the lane
+                // crosses at most one structure, the next record in the table
+                beta_i += dB;
+                alpha_i += dA;
+                if (beta_i >= nB) {
+                    beta_i -= nB;
+                    alpha_i++;
+                }
+                if (alpha_i >= nA) {
+                    alpha_i -= nA;
+                    sidx++;
+                    load_rec(w, sidx, m);
+                }
+            } else if (j < nsteps && (uint32_t)lane + 32u * j < len) {
                 // step into the next configuration: generic odometer (may leave the block)
                 L.d[D_ALPHA] = alpha_i;
                 L.d[D_BETA] = beta_i;
                 const int lvl = advance(w, v, L, cuts, cs);
                 if (lvl >= D_LS) {
-                    if (PIPE && lvl >= D_PART)
-                        stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
-                    compute_mid<FAM>(v, L, st, m, w.halo);
-                    if (GP) gpipe_fill(v, L, cuts, cs, m);
-                    fastify(m);
+                    if (rec) {
+                        sidx = struct_index(v, L);
+                        load_rec(w, sidx, m);
+                    } else {
+                        if (PIPE && lvl >= D_PART)
+                            stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+                        compute_mid<FAM>(v, L, st, m, w.halo);
+                        if (GP) gpipe_fill(v, L, cuts, cs, m);
+                        fastify(m);
+                    }
                 }
                 alpha_i = L.d[D_ALPHA];
                 beta_i = L.d[D_BETA];
@@ -2646,6 +2700,43 @@ cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st) {
     const int blocks = (int)((warps * 32 + threads - 1) / threads);
     void *args[] = {const_cast<HaloJobs *>(&jobs)};
     return cudaLaunchKernel((void *)halo_table_kernel, dim3(blocks), dim3(threads), args, 0, st);
+}
+
+// ------------------------------------------------------------------ pipeline structure table
+// One thread per structure (cap, R, b, partition, S, dims, Ls) of a pipeline sub-sweep: the
+// structure terms the mode-0 tiles would otherwise recompute once per warp and structure
+// (decode, stage sums, compute_mid<PIPELINE>, fastify) -- the same device code, 32
+// structures per warp instruction.  The image is read from global memory (L1/L2 cached).
+__global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, const StructJob job) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= job.n) return;
+    const View v = make_view(img, job.sub);
+    const uint64_t nAB = (uint64_t)v.S->radix[D_ALPHA] * v.S->radix[D_BETA];
+    uint16_t cuts[kMaxCuts + 1];
+    Lane L;
+    decode(v, (job.s_lo + i) * nAB, L, cuts, 1);
+    StageT st;
+    stage_terms(v, L, cuts, 1, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+    Mid m;
+    m.reset_memo();
+    compute_mid<PARADL_PIPELINE>(v, L, st, m);
+    fastify(m);
+    PipeRec r;
+    r.comp = m.comp;
+    r.pp_c = m.pp_c;
+    r.pp_s = m.pp_s;
+    r.I = m.I;
+    r.reason = m.reason;
+    r.pp_t = m.pp_t;
+    r.pad[0] = r.pad[1] = 0;
+    job.out[i] = r;
+}
+
+cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, cudaStream_t st) {
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((job.n + threads - 1) / threads);
+    struct_table_kernel<<<blocks, threads, 0, st>>>(img, job);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ FP64 peak microbenchmark

@@ -99,6 +99,25 @@ struct WorkItem {
     uint32_t memo_off, memo_n;     // mode 1/2: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
     uint32_t low_off, flags;       // mode 2: index of its [n_b][256] low-bit stage table (LowE units);
                                    // flags: kWorkMaskD = screened pipeline masks, stage terms as exact doubles
+    const struct PipeRec *stab;    // mode 0 pipeline, reduce: structure table (device global), else null
+    uint64_t stab_lo;              // structure index of stab[0] within the sub-sweep
+};
+
+// Structure record of a pipeline sub-sweep (reduce mode): the alpha/beta-invariant terms of
+// compute_mid<PIPELINE> + fastify for one structure (cap, R, b, partition, S, dims, Ls),
+// written by the structure-table kernel, read by the sweep kernel's mode-0 tiles.
+struct PipeRec {
+    double comp, pp_c, pp_s, I;
+    uint32_t reason;
+    int32_t pp_t;
+    uint32_t pad[2];
+};
+static_assert(sizeof(PipeRec) == 48, "PipeRec layout");
+
+struct StructJob {
+    int32_t sub, pad;
+    uint64_t s_lo, n;              // structures [s_lo, s_lo + n) of sub-sweep `sub`
+    PipeRec *out;
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
@@ -148,6 +167,7 @@ cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *gbound = nullptr, int32_t lstride = 0, int32_t cstride = 0,
                          unsigned long long *bound_out = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
+cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
 cudaError_t launch_explain(const uint8_t *img, uint32_t img_bytes, int32_t sub, uint64_t local,
                            paradl_config *d_cfg, paradl_prediction *d_pred, cudaStream_t st);
