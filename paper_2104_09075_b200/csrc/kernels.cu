@@ -2708,33 +2708,47 @@ cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st) {
 // (decode, stage sums, compute_mid<PIPELINE>, fastify) -- the same device code, 32
 // structures per warp instruction.  The image is read from global memory (L1/L2 cached).
 __global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, const StructJob job) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= job.n) return;
+    // one thread per (cap, R, b, partition) unit: the partition is unranked and its stage
+    // sums formed once, then the unit's S x dims x Ls structures are emitted
     const View v = make_view(img, job.sub);
-    const uint64_t nAB = (uint64_t)v.S->radix[D_ALPHA] * v.S->radix[D_BETA];
+    const SubHdr *S = v.S;
+    const uint32_t nL = S->radix[D_LS], nD = S->radix[D_DIMS], nS = S->radix[D_S];
+    const uint64_t K = (uint64_t)nS * nD * nL;
+    const uint64_t unit = job.s_lo / K + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t s_hi = job.s_lo + job.n;
+    if (unit * K >= s_hi) return;
+    const uint64_t nAB = (uint64_t)S->radix[D_ALPHA] * S->radix[D_BETA];
     uint16_t cuts[kMaxCuts + 1];
     Lane L;
-    decode(v, (job.s_lo + i) * nAB, L, cuts, 1);
+    decode(v, unit * K * nAB, L, cuts, 1);
     StageT st;
-    stage_terms(v, L, cuts, 1, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+    stage_terms(v, L, cuts, 1, at<int64_t>(v.img, S->off_b)[L.d[D_B]], st);
     Mid m;
     m.reset_memo();
-    compute_mid<PARADL_PIPELINE>(v, L, st, m);
-    fastify(m);
-    PipeRec r;
-    r.comp = m.comp;
-    r.pp_c = m.pp_c;
-    r.pp_s = m.pp_s;
-    r.I = m.I;
-    r.reason = m.reason;
-    r.pp_t = m.pp_t;
-    r.pad[0] = r.pad[1] = 0;
-    job.out[i] = r;
+    for (uint64_t k = 0; k < K; k++) {
+        const uint64_t s = unit * K + k;
+        if (s < job.s_lo || s >= s_hi) continue;
+        L.d[D_LS] = (uint32_t)(k % nL);
+        L.d[D_DIMS] = (uint32_t)((k / nL) % nD);
+        L.d[D_S] = (uint32_t)(k / ((uint64_t)nL * nD));
+        compute_mid<PARADL_PIPELINE>(v, L, st, m);
+        fastify(m);
+        PipeRec r;
+        r.comp = m.comp;
+        r.pp_c = m.pp_c;
+        r.pp_s = m.pp_s;
+        r.I = m.I;
+        r.reason = m.reason;
+        r.pp_t = m.pp_t;
+        r.pad[0] = r.pad[1] = 0;
+        job.out[s - job.s_lo] = r;
+    }
 }
 
-cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, cudaStream_t st) {
+cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, uint64_t unit_len, cudaStream_t st) {
     const int threads = 256;
-    const unsigned blocks = (unsigned)((job.n + threads - 1) / threads);
+    const uint64_t units = (job.s_lo + job.n + unit_len - 1) / unit_len - job.s_lo / unit_len;
+    const unsigned blocks = (unsigned)((units + threads - 1) / threads);
     struct_table_kernel<<<blocks, threads, 0, st>>>(img, job);
     return cudaGetLastError();
 }
