@@ -63,7 +63,7 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one, halo, stab;
+    DevBuf img, lists, counters, results, one, halo, stab, nvalid;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
     std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
@@ -897,6 +897,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     }
     CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 2)));
     if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * total_ctas * k));
+    if (!dense) CUDA_TRY(c, c->nvalid.ensure(sizeof(uint32_t) * total_ctas));
     unsigned long long *ctr = (unsigned long long *)c->counters.p;
     CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
     CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
@@ -938,6 +939,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         a.gbound = ctr + nl + 1;
         a.k = k;
         a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
+        a.cta_nvalid = dense ? nullptr : (uint32_t *)c->nvalid.p + cta_off;
         if (dense) {
             a.t_iter = out->t_iter;
             a.mem = out->mem;
@@ -1006,7 +1008,8 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
         CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     }
     CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
-                             (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr));
+                             (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr, 0, 0,
+                             nullptr, nlists ? (const uint32_t *)c->nvalid.p : nullptr));
     c->stat_launches++;
     return PARADL_OK;
 }

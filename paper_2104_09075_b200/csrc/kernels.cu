@@ -2344,9 +2344,21 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1 : PARADL_
         if (lane == 0) atomicAdd(&s_count, cnt);
         __syncthreads();
         bitonic_sort_smem(lst, kWarps * PARADL_MAX_TOPK);
+        // entries above the shared admission bound (some warp's k-th key) can never reach
+        // the global top k: only the sorted prefix at or below it is written and counted
+        double gk = CUDART_INF;
+        if (a.gbound) {
+            const unsigned long long g = *(volatile unsigned long long *)a.gbound;
+            if (g != ~0ull) gk = __longlong_as_double((long long)g);
+        }
+        const int nv = __syncthreads_count(threadIdx.x < (unsigned)a.k && lst[threadIdx.x].idx != ~0ull &&
+                                           lst[threadIdx.x].key_epoch_s <= gk);
         paradl_hit *out = a.cta_lists + (size_t)blockIdx.x * a.k;
-        for (int i = threadIdx.x; i < a.k; i += blockDim.x) out[i] = lst[i];
-        if (threadIdx.x == 0) atomicAdd(a.count, s_count);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) out[i] = lst[i];
+        if (threadIdx.x == 0) {
+            a.cta_nvalid[blockIdx.x] = (uint32_t)nv;
+            atomicAdd(a.count, s_count);
+        }
     }
 }
 
@@ -2368,7 +2380,8 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
                                                       const unsigned long long *counts, int32_t n_counts,
                                                       paradl_hit *out, unsigned long long *count_out,
                                                       const unsigned long long *gbound, int32_t lstride,
-                                                      int32_t cstride, unsigned long long *bound_out) {
+                                                      int32_t cstride, unsigned long long *bound_out,
+                                                      const uint32_t *nvalid) {
     __shared__ paradl_hit cand[kMergeCand];
     __shared__ unsigned long long s_cnt;
     __shared__ double s_wk[32];
@@ -2387,8 +2400,11 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     // 1. bound: smallest k-th entry over the lists
     double bk = CUDART_INF;
     uint64_t bi = ~0ull;
+    // (nvalid: list l holds only its first nvalid[l] entries -- the sweep kernel dropped
+    // the rest as above its admission bound)
     for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x)
-        hit_min(bk, bi, lists[l * lstride + (k - 1)].key_epoch_s, lists[l * lstride + (k - 1)].idx);
+        if (!nvalid || nvalid[l] == (uint32_t)k)
+            hit_min(bk, bi, lists[l * lstride + (k - 1)].key_epoch_s, lists[l * lstride + (k - 1)].idx);
     for (int o = 16; o; o >>= 1) hit_min(bk, bi, __shfl_xor_sync(full, bk, o), __shfl_xor_sync(full, bi, o));
     if (lane == 0) {
         s_wk[warp] = bk;
@@ -2416,12 +2432,25 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     // 2. candidates <= bound: one thread per entry (independent, coalesced loads; a per-list
     //    walk would chain one global-memory latency per entry)
     const int64_t n_ent = n_lists * (int64_t)k;
-    for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
-        const int64_t l = e / k, j = e - l * k;
-        const paradl_hit h = lists[l * lstride + j];
-        if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
-        const int pos = atomicAdd(&s_nc, 1);
-        if (pos < kMergeCand) cand[pos] = h;
+    if (nvalid) {
+        // pruned lists hold few entries: one thread per list walks its valid prefix
+        for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
+            const int nv = (int)nvalid[l];
+            for (int j = 0; j < nv; j++) {
+                const paradl_hit h = lists[l * lstride + j];
+                if (hit_less(bk, bi, h.key_epoch_s, h.idx)) break;   // sorted: the rest is larger
+                const int pos = atomicAdd(&s_nc, 1);
+                if (pos < kMergeCand) cand[pos] = h;
+            }
+        }
+    } else {
+        for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
+            const int64_t l = e / k, j = e - l * k;
+            const paradl_hit h = lists[l * lstride + j];
+            if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
+            const int pos = atomicAdd(&s_nc, 1);
+            if (pos < kMergeCand) cand[pos] = h;
+        }
     }
     __syncthreads();
     const int nc = s_nc;
@@ -2453,7 +2482,7 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
         for (int64_t e = 0; e < n; e += 32) {
             const int64_t j = e + lane;
             const int64_t jj = (j / k) * lstride + (j % k);
-            const bool ok = j < n && lists[jj].idx != ~0ull;
+            const bool ok = j < n && (!nvalid || (j % k) < (int64_t)nvalid[j / k]) && lists[jj].idx != ~0ull;
             tk.offer(ok, ok ? lists[jj].key_epoch_s : CUDART_INF, ok ? lists[jj].idx : ~0ull);
         }
     }
@@ -2862,9 +2891,9 @@ cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, i
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k, const unsigned long long *counts,
                          int32_t n_counts, paradl_hit *out, unsigned long long *count_out, cudaStream_t st,
                          const unsigned long long *gbound, int32_t lstride, int32_t cstride,
-                         unsigned long long *bound_out) {
+                         unsigned long long *bound_out, const uint32_t *nvalid) {
     merge_kernel<<<1, 1024, 0, st>>>(lists, n_lists, k, counts, n_counts, out, count_out, gbound,
-                                     lstride > 0 ? lstride : k, cstride > 0 ? cstride : 1, bound_out);
+                                     lstride > 0 ? lstride : k, cstride > 0 ? cstride : 1, bound_out, nvalid);
     return cudaGetLastError();
 }
 

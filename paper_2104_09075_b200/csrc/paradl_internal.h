@@ -134,6 +134,7 @@ struct LaunchArgs {
     int32_t k;
     uint32_t dtab_bytes;           // mode-1 screened path: per-lane dims tables after the low tables
     paradl_hit *cta_lists;         // [gridDim.x][k] (reduce mode)
+    uint32_t *cta_nvalid;          // [gridDim.x] entries written per CTA list (reduce mode)
     unsigned long long *count;     // feasible count accumulator (reduce mode)
     unsigned long long *gbound;    // shared top-k admission bound (reduce mode; ~0 = none)
     double *t_iter;                // dense outputs (indexed by global idx - first)
@@ -165,7 +166,7 @@ cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
                          unsigned long long *count_out, cudaStream_t st,
                          const unsigned long long *gbound = nullptr, int32_t lstride = 0, int32_t cstride = 0,
-                         unsigned long long *bound_out = nullptr);
+                         unsigned long long *bound_out = nullptr, const uint32_t *nvalid = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
 cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, uint64_t unit_len, cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
