@@ -2367,7 +2367,8 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1 : PARADL_
 // paradl_topk_async) and sums n_counts counts.  The k-th entry of any full list bounds
 // the k-th global entry, so only entries <= the smallest such bound can survive: one
 // thread per list collects them (early exit, lists are sorted), then one warp selects.
-constexpr int kMergeCand = 2048;
+constexpr int kMergeCand = 1536;
+constexpr int kMergeLists = 4096;   // lists whose valid-prefix offsets fit the shared scan
 
 __device__ __forceinline__ void hit_min(double &k, uint64_t &i, double k2, uint64_t i2) {
     if (hit_less(k2, i2, k, i)) {
@@ -2383,6 +2384,7 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
                                                       int32_t cstride, unsigned long long *bound_out,
                                                       const uint32_t *nvalid) {
     __shared__ paradl_hit cand[kMergeCand];
+    __shared__ uint32_t s_pre[kMergeLists + 1];
     __shared__ unsigned long long s_cnt;
     __shared__ double s_wk[32];
     __shared__ uint64_t s_wi[32];
@@ -2432,8 +2434,43 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     // 2. candidates <= bound: one thread per entry (independent, coalesced loads; a per-list
     //    walk would chain one global-memory latency per entry)
     const int64_t n_ent = n_lists * (int64_t)k;
-    if (nvalid) {
-        // pruned lists hold few entries: one thread per list walks its valid prefix
+    if (nvalid && n_lists <= kMergeLists) {
+        // pruned lists: exclusive prefix of the valid counts (warp 0, lane-chunked scan),
+        // then one thread per valid entry (independent loads, one memory latency)
+        for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) s_pre[l + 1] = nvalid[l];
+        __syncthreads();
+        if (warp == 0) {
+            const int nl = (int)n_lists, per = (nl + 31) / 32, b0 = min(nl, lane * per), b1 = min(nl, b0 + per);
+            uint32_t sum = 0;
+            for (int l = b0; l < b1; l++) sum += s_pre[l + 1];
+            uint32_t inc = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(full, inc, o);
+                if (lane >= o) inc += v;
+            }
+            uint32_t run = inc - sum;
+            for (int l = b0; l < b1; l++) {
+                const uint32_t v = s_pre[l + 1];
+                s_pre[l] = run;
+                run += v;
+            }
+            if (lane == 31) s_pre[nl] = inc;
+        }
+        __syncthreads();
+        const uint32_t V = s_pre[n_lists];
+        for (uint32_t e = threadIdx.x; e < V; e += blockDim.x) {
+            int lo = 0, hi = (int)n_lists;   // last list with s_pre[l] <= e
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= e) lo = mid;
+                else hi = mid;
+            }
+            const paradl_hit h = lists[(int64_t)lo * lstride + (e - s_pre[lo])];
+            if (hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
+            const int pos = atomicAdd(&s_nc, 1);
+            if (pos < kMergeCand) cand[pos] = h;
+        }
+    } else if (nvalid) {
         for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
             const int nv = (int)nvalid[l];
             for (int j = 0; j < nv; j++) {
@@ -2455,22 +2492,25 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     __syncthreads();
     const int nc = s_nc;
     if (nc <= kMergeCand) {
-        // sort the candidates (padded to a power of two) and keep the first k
-        int n2 = 64;   // >= k (k <= 64) so that out[] never reads unsorted slots
-        while (n2 < nc) n2 <<= 1;
-        for (int i = nc + threadIdx.x; i < n2; i += blockDim.x) {
-            cand[i].idx = ~0ull;
-            cand[i].key_epoch_s = CUDART_INF;
+        // rank selection: (key, idx) pairs are distinct, so a candidate's rank is the number
+        // of candidates before it; ranks < k go straight to their output slot (one pass,
+        // broadcast shared-memory reads, no sorting network)
+        for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+            const paradl_hit h = cand[i];
+            int r = 0;
+            for (int j = 0; j < nc; j++) r += hit_less(cand[j].key_epoch_s, cand[j].idx, h.key_epoch_s, h.idx);
+            if (r < k) {
+                if (out) out[r] = h;
+                if (r == k - 1 && bound_out)
+                    atomicMin(bound_out, (unsigned long long)__double_as_longlong(h.key_epoch_s));
+            }
         }
-        __syncthreads();
-        bitonic_sort_smem(cand, n2);
         if (out)
-            for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = cand[i];
-        if (threadIdx.x == 0) {
-            if (count_out) *count_out = s_cnt;
-            if (bound_out && cand[k - 1].idx != ~0ull)
-                atomicMin(bound_out, (unsigned long long)__double_as_longlong(cand[k - 1].key_epoch_s));
-        }
+            for (int i = nc + threadIdx.x; i < k; i += blockDim.x) {
+                out[i].idx = ~0ull;
+                out[i].key_epoch_s = CUDART_INF;
+            }
+        if (threadIdx.x == 0 && count_out) *count_out = s_cnt;
         return;
     }
     if (warp != 0) return;
