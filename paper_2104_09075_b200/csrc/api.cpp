@@ -909,7 +909,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     for (const StructJob &j : sjobs) {
         const SubHdr &h = P.subs[j.sub].hdr;
         const uint64_t unit_len = (uint64_t)h.radix[D_S] * h.radix[D_DIMS] * h.radix[D_LS];
-        CUDA_TRY(c, launch_struct_table((const uint8_t *)c->img.p, j, unit_len, st));
+        CUDA_TRY(c, launch_struct_table((const uint8_t *)c->img.p, P.bytes, j, unit_len, st));
         c->stat_launches++;
     }
     // fork onto internal streams

@@ -2776,10 +2776,14 @@ cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st) {
 // structure terms the mode-0 tiles would otherwise recompute once per warp and structure
 // (decode, stage sums, compute_mid<PIPELINE>, fastify) -- the same device code, 32
 // structures per warp instruction.  The image is read from global memory (L1/L2 cached).
-__global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, const StructJob job) {
+__global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, uint32_t img_bytes, const StructJob job) {
     // one thread per (cap, R, b, partition) unit: the partition is unranked and its stage
-    // sums formed once, then the unit's S x dims x Ls structures are emitted
-    const View v = make_view(img, job.sub);
+    // sums formed once, then the unit's S x dims x Ls structures are emitted; the image is
+    // staged into shared memory first (one TMA bulk copy, as in the sweep kernels)
+    extern __shared__ __align__(128) uint8_t simg[];
+    __shared__ uint64_t mbar;
+    stage_image(simg, img, img_bytes, &mbar);
+    const View v = make_view(simg, job.sub);
     const SubHdr *S = v.S;
     const uint32_t nL = S->radix[D_LS], nD = S->radix[D_DIMS], nS = S->radix[D_S];
     const uint64_t K = (uint64_t)nS * nD * nL;
@@ -2814,11 +2818,15 @@ __global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, c
     }
 }
 
-cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, uint64_t unit_len, cudaStream_t st) {
+static cudaError_t ensure_smem_attr(void *fn, size_t smem);
+cudaError_t launch_struct_table(const uint8_t *img, uint32_t img_bytes, const StructJob &job, uint64_t unit_len,
+                                cudaStream_t st) {
     const int threads = 256;
     const uint64_t units = (job.s_lo + job.n + unit_len - 1) / unit_len - job.s_lo / unit_len;
     const unsigned blocks = (unsigned)((units + threads - 1) / threads);
-    struct_table_kernel<<<blocks, threads, 0, st>>>(img, job);
+    cudaError_t e = ensure_smem_attr((void *)struct_table_kernel, img_bytes);
+    if (e != cudaSuccess) return e;
+    struct_table_kernel<<<blocks, threads, img_bytes, st>>>(img, img_bytes, job);
     return cudaGetLastError();
 }
 

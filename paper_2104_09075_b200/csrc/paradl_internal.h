@@ -168,7 +168,8 @@ cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *gbound = nullptr, int32_t lstride = 0, int32_t cstride = 0,
                          unsigned long long *bound_out = nullptr, const uint32_t *nvalid = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
-cudaError_t launch_struct_table(const uint8_t *img, const StructJob &job, uint64_t unit_len, cudaStream_t st);
+cudaError_t launch_struct_table(const uint8_t *img, uint32_t img_bytes, const StructJob &job, uint64_t unit_len,
+                                cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
 cudaError_t launch_explain(const uint8_t *img, uint32_t img_bytes, int32_t sub, uint64_t local,
                            paradl_config *d_cfg, paradl_prediction *d_pred, cudaStream_t st);
