@@ -22,6 +22,17 @@
 
 namespace paradl {
 
+// tuning knobs (experiments build variants with -D; defaults are the measured best)
+#ifndef PARADL_MINB
+#define PARADL_MINB 2
+#endif
+#ifndef PARADL_PIPE_MINB
+#define PARADL_PIPE_MINB PARADL_MINB
+#endif
+#ifndef PARADL_PIPE_KEYS
+#define PARADL_PIPE_KEYS 16
+#endif
+
 // ------------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -1160,7 +1171,8 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
     // R = KEYS/M whole alpha rows per iteration: KEYS independent dependency chains (16 for
     // the light families, 8 where more comm terms would spill); the admission test is one
     // ballot per key (no min/select sequence)
-    constexpr int KEYS = (FAM == PARADL_PIPELINE || FAM == PARADL_DATA || FAM == PARADL_LAYERPURE) ? 16
+    constexpr int KEYS = FAM == PARADL_PIPELINE                                ? PARADL_PIPE_KEYS
+                         : (FAM == PARADL_DATA || FAM == PARADL_LAYERPURE) ? 16
                          : (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_DF ||
                             FAM == PARADL_SPATIAL_AG)                                             ? 4
                                                                                                   : 8;
@@ -2286,11 +2298,11 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
     __syncthreads();
 }
 
-#ifndef PARADL_MINB
-#define PARADL_MINB 2
-#endif
 template <int FAM, bool DENSE, int BLK>
-__global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1 : PARADL_MINB) sweep_kernel(const __grid_constant__ LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
+                                            : (FAM == PARADL_PIPELINE && !DENSE && BLK == 0) ? PARADL_PIPE_MINB
+                                                                                             : PARADL_MINB)
+    sweep_kernel(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ unsigned long long s_count;
