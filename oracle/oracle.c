@@ -542,6 +542,32 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (S < 1 || S > b) reason |= OR_R_SEGMENTS;   /* S <= B (Q9) */
         break;
     }
+    case OR_DATA_LW: {
+        /* Data row of Table 2 with the gradient exchanged as one Allreduce per
+         * weighted layer (message delta |w_l|, row order), each message sent with the ring
+         * algorithm when large and the tree algorithm when small: "ring-based algorithm for
+         * ... large message sizes and a tree-based algorithm for small message sizes"
+         * (P:552), tree time of the footnote (Q37).  GE = left fold over the layers. */
+        p = d[0];
+        if (d[1] != 1 || d[2] != 1 || d[3] != 1) FAIL(E_INVAL, "data_lw dims are (p,1,1,1)");
+        if (!mul_ok(b, p, &B)) FAIL(E_OVERFLOW, "b*p");
+        if (!mul_ok(B, s.FB, &BFB) || !mul_ok(2 * B, s.XY, &twoBXY)) FAIL(E_OVERFLOW, "B*FB");
+        comp = comp_term(BFB, s.WU, p, 1, tau);
+        int t = tier_or_flag(sys, p, &reason);
+        if (t < 0) {
+            ge = INFINITY;
+        } else {
+            for (int64_t l = 0; l < m->G; l++) {
+                const int64_t w = m->rows[l].w;
+                if (w <= 0) continue;
+                const double ml = (double)(delta * w);
+                ge = ge + t_allreduce(sys, p, ml, ml / (double)p, c->alpha[t], c->beta[t]);
+            }
+        }
+        mem = mem_term(sys, twoBXY, s.W, s.BI, p, 1);
+        if (p > B) reason |= OR_R_SCALING;
+        break;
+    }
     case OR_SPATIAL_AG: {
         /* "we implement the spatial strategy for some first layers ... We then
          * implement an Allgather to collect the full set of activations before passing
@@ -701,7 +727,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
     int64_t B = o->B, p = o->p;
     int64_t pc = 1, pu = 1, pa = 1, pw = 1;
     int fam = c->family;
-    if (fam == OR_DATA) { pc = p; pa = p; }
+    if (fam == OR_DATA || fam == OR_DATA_LW) { pc = p; pa = p; }
     if (fam == OR_SPATIAL || fam == OR_DS) { pc = p; pa = p; }
     if (fam == OR_FILTER || fam == OR_CHANNEL) { pc = p; pu = p; pw = p; }
     if (fam == OR_DF) { pc = p; pu = d[1]; pa = d[0]; pw = d[1]; }
@@ -735,7 +761,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
             o->t_fb_ag = (double)(p - 1) * (c->alpha[t] + (double)B * (double)m->rows[Lp - 1].y / (double)p * dl * c->beta[t]);
         }
     }
-    if (fam == OR_SERIAL || fam == OR_DATA || fam == OR_SPATIAL || fam == OR_DS ||
+    if (fam == OR_SERIAL || fam == OR_DATA || fam == OR_DATA_LW || fam == OR_SPATIAL || fam == OR_DS ||
         fam == OR_FILTER || fam == OR_CHANNEL || fam == OR_DF || fam == OR_LAYERPURE) {
         int64_t Bc = fam == OR_LAYERPURE ? b : B;
         double comp = 0.0;

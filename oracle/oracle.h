@@ -25,6 +25,8 @@ enum { OR_SERIAL = 0, OR_DATA, OR_SPATIAL, OR_FILTER, OR_CHANNEL, OR_DF, OR_DS,
        OR_PIPELINE, OR_LAYERPURE, OR_PD,
        OR_SPATIAL_AG,   /* spatial on the first Ls rows, Allgather, replicated rest (Q35) */
        OR_GPIPE,        /* pipeline timed by the GPipe schedule itself (Q36) */
+       OR_DATA_LW,      /* data parallel, one gradient Allreduce per weighted layer, each message
+                         * ring or tree by its size (Q37) */
        OR_N_FAMILIES };
 enum { OR_PART_NONE = 0, OR_PART_COMB = 1, OR_PART_MASK = 2 };
 /* infeasibility reasons (bit set) */

@@ -172,6 +172,17 @@ def exact(sweep, cfg):
             al = inf if to is None else ar_exact(sys, p1, Fr(dl * W_), Fr(dl * W_, p1), A[to], Bt[to])
             ge = inf if (rl is None or al is None) else rl + al
         mem = mem_row(B, p, 1)
+    elif fam == W.DATA_LW:
+        # data parallelism, one Allreduce per weighted layer, ring or tree per message (Q37)
+        p = p1
+        B = b * p
+        comp = comp_row(B, p, 1)
+        t = tier(p)
+        ge = inf if t is None else sum(ar_exact(sys, p, Fr(dl * r.w), Fr(dl * r.w, p), A[t], Bt[t])
+                                       for r in L if r.w > 0)
+        mem = mem_row(B, p, 1)
+        if p > B:
+            reason |= R_SCALING
     elif fam == W.SPATIAL_AG:
         # spatial on rows [0, Ls), Allgather of y_Ls, rows [Ls, G) replicated (Q35)
         split = (d1, d2, d3)
@@ -376,11 +387,22 @@ def buffer_bytes(sweep, cfg):
 
     if fam == W.SERIAL:
         tot = sum(layer_bufs(r, b, 1, 1) for r in L)
-    elif fam == W.DATA:
+    elif fam in (W.DATA, W.DATA_LW):
         tot = sum(layer_bufs(r, b * p1, p1, 1) for r in L)          # B' = B/p samples
     elif fam in (W.SPATIAL, W.DS):
         p2 = d1 * d2 * d3
         tot = sum(layer_bufs(r, b * p1, p1 * p2, 1) for r in L)     # spatial shard of the group batch
+    elif fam == W.DATA_LW:
+        # data parallelism, one Allreduce per weighted layer, ring or tree per message (Q37)
+        p = p1
+        B = b * p
+        comp = comp_row(B, p, 1)
+        t = tier(p)
+        ge = inf if t is None else sum(ar_exact(sys, p, Fr(dl * r.w), Fr(dl * r.w, p), A[t], Bt[t])
+                                       for r in L if r.w > 0)
+        mem = mem_row(B, p, 1)
+        if p > B:
+            reason |= R_SCALING
     elif fam == W.SPATIAL_AG:
         p2 = d1 * d2 * d3
         Lp = min(cfg["Ls"], len(L))

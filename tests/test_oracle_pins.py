@@ -435,6 +435,47 @@ def test_spatial_ag_limits(oracle_mod):
                 prev = z
 
 
+# ------------------------------------------------------------ per-layer gradient messages (Q37)
+def test_data_lw_reduces_to_table2(oracle_mod):
+    """Ring only: one Allreduce per weighted layer costs Table 2's data GE plus one extra
+    startup 2(p-1) alpha per additional message, exactly (rationals); a model with one
+    weighted layer is the Data row bit for bit; compute and memory are the Data row's."""
+    rng = random.Random(21)
+    for trial in range(60):
+        n = rng.randint(1, 6)
+        ws = [rng.choice([0, rng.randint(1, 5000)]) for _ in range(n)]
+        if not any(ws):
+            ws[0] = 7
+        rows = [toys.row(w=w, fw=rng.randint(1, 99), bw=rng.randint(1, 99), x=3, y=5) for w in ws]
+        m = toys.model(rows, D=1000)
+        p = rng.choice([1, 2, 3, 4, 8, 64])
+        a, be = rng.choice([1e-6, 3e-5]), rng.choice([1e-9, 5e-10])
+        sysm = toys.system(delta=4)
+        sub = dict(b=[4], dims=[(p, 1, 1, 1)], alpha=[[a]], beta=[[be]])
+        lw = _one(oracle_mod, m, sysm, W.SubSweep(W.DATA_LW, **sub))
+        dp = _one(oracle_mod, m, sysm, W.SubSweep(W.DATA, **sub))
+        nw = sum(1 for w in ws if w > 0)
+        want = Fr(dp.t_ge) + (nw - 1) * 2 * (p - 1) * Fr(a) if p > 1 else Fr(0)
+        assert _rel(lw.t_ge, want) <= 1e-14
+        assert lw.t_comp == dp.t_comp and lw.mem == dp.mem and lw.reason == dp.reason
+        if nw == 1:
+            assert lw.t_ge == dp.t_ge and lw.t_iter == dp.t_iter
+
+
+def test_data_lw_per_message_dispatch(oracle_mod):
+    """Each message is timed by the tree form when smaller than the threshold and by the
+    ring otherwise: a small and a large layer straddling the threshold give
+    tree(small) + ring(large), checked against the explicit ring simulation."""
+    rows = [toys.row(w=100), toys.row(w=1_000_000)]
+    m = toys.model(rows, D=10)
+    a, be, p, k = 2e-6, 1e-9, 8, 4
+    sysm = toys.system(delta=4, tree_threshold=1e5, tree_chunks=k)
+    lw = _one(oracle_mod, m, sysm, W.SubSweep(W.DATA_LW, b=[2], dims=[(p, 1, 1, 1)], alpha=[[a]], beta=[[be]]))
+    tree_small = 2 * (3 + k) * (Fr(a) + Fr(400, 2 * k) * Fr(be))
+    ring_large, _ = brute.ring_allreduce_sim(p, Fr(4_000_000), Fr(a), Fr(be))
+    assert _rel(lw.t_ge, tree_small + ring_large) <= 1e-15
+
+
 # ------------------------------------------------------------ memory
 @pytest.mark.parametrize("seed", range(25))
 def test_memory_rows_equal_buffer_enumeration(oracle_mod, seed):

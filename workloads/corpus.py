@@ -81,7 +81,7 @@ def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:
         return A, B
 
     subs = []
-    fams = list(range(12))
+    fams = list(range(13))
     rng.shuffle(fams)
     for fam in fams:
         mi = rng.randint(0, 1)
@@ -91,7 +91,7 @@ def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:
                   b=some([1, 2, 3, 4, 8, 16, 32]),
                   cap=some([2.0 ** 18, 2.0 ** 24, 2.0 ** 30]) if rng.random() < 0.5 else [],
                   flops=some([1e12, 2.5e12]) if rng.random() < 0.5 else [])
-        if fam in (W.DATA, W.FILTER, W.CHANNEL):
+        if fam in (W.DATA, W.FILTER, W.CHANNEL, W.DATA_LW):
             kw["dims"] = [(p, 1, 1, 1) for p in some([1, 2, 3, 4, 8, 16, 64, 1024])]
         elif fam == W.DF:
             kw["dims"] = [(rng.choice([1, 2, 3, 4]), rng.choice([1, 2, 4, 5]), 1, 1) for _ in range(rng.randint(1, 3))]

@@ -18,8 +18,10 @@ from . import models as M
 SERIAL, DATA, SPATIAL, FILTER, CHANNEL, DF, DS, PIPELINE, LAYERPURE, PD = range(10)
 # SURVEY §8(f) "next" rows: spatial prefix + Allgather, GPipe schedule
 SPATIAL_AG, GPIPE = 10, 11
+# per-layer gradient messages with per-message ring / tree dispatch
+DATA_LW = 12
 FAMILY_NAMES = ["serial", "data", "spatial", "filter", "channel", "df", "ds",
-                "pipeline", "layerpure", "pd", "spatial_ag", "gpipe"]
+                "pipeline", "layerpure", "pd", "spatial_ag", "gpipe", "data_lw"]
 PIPE_FAMILIES = (PIPELINE, LAYERPURE, PD, GPIPE)
 SPATIAL_FAMILIES = (SPATIAL, DS, SPATIAL_AG)
 
