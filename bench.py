@@ -494,6 +494,18 @@ def next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak):
                     off += blk[j]
             opc = ops / max(1, n_feas)
             kern = "sweep_kernel<GPIPE,reduce>"
+        elif name == "data_lw":
+            # per configuration: 4 FP64 per weighted layer (s*beta, alpha+, c*, fold +), comp +
+            # GE, key * I; exact per sub-sweep (models differ in weighted layers)
+            ops = 0.0
+            for si, sb in enumerate(sw.subs):
+                lw = sum(1 for r in sw.models[sb.model].layers if r.w > 0)
+                sub_spec = P.Spec([sb], [spec.c.sub[si].model_id])
+                _, c = ctx.topk(sub_spec, 1, 0, ctx.sweep_size(sub_spec))
+                ops += c * (4.0 * lw + 2.0)
+            ctx.prepare(sw)
+            opc = ops / max(1, n_feas)
+            kern = "sweep_kernel<DATA_LW,reduce>"
         else:
             opc = FP64_OPS_PER_CONFIG["spatial_ag"]   # GE 3 + Allgather 3 + halo 3 + 1/M + key 1
             ops = opc * n_feas

@@ -66,10 +66,14 @@ enum { PARADL_FLAG_COMM = 1u, PARADL_FLAG_FOLDED = 4u };
  * GPIPE: a pipeline partition timed by the GPipe schedule itself (S segments, forward
  *   wave then backward wave, blocking boundary sends, per-stage WU, DESIGN.md
  *   Q36) instead of Table 2's max-stage form.  Needs s <= PARADL_GPIPE_MAX_STAGES
- *   (COMB: s_max, MASK: G) and S >= 1. */
+ *   (COMB: s_max, MASK: G) and S >= 1.
+ * DATA_LW: dims (p,1,1,1); the Data row with the gradient exchanged as one Allreduce per
+ *   weighted layer (message delta |w_l|, row order), each message ring or tree by its size
+ *   against tree_threshold_B ("ring ... for large message sizes and a tree-based algorithm
+ *   for small message sizes"; tree time P:559; Q37). */
 enum { PARADL_SERIAL = 0, PARADL_DATA, PARADL_SPATIAL, PARADL_FILTER, PARADL_CHANNEL,
        PARADL_DF, PARADL_DS, PARADL_PIPELINE, PARADL_LAYERPURE, PARADL_PD,
-       PARADL_SPATIAL_AG, PARADL_GPIPE, PARADL_N_FAMILIES };
+       PARADL_SPATIAL_AG, PARADL_GPIPE, PARADL_DATA_LW, PARADL_N_FAMILIES };
 #define PARADL_GPIPE_MAX_STAGES 8
 
 /* Partition radix of the pipeline families (groups g_i, P:519 footnote).

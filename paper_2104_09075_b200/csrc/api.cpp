@@ -374,14 +374,17 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
             switch (fam) {
             case PARADL_SERIAL: case PARADL_PIPELINE: case PARADL_LAYERPURE: case PARADL_GPIPE:
                 ok = d[0] == 1 && d[1] == 1 && d[2] == 1 && d[3] == 1; break;
-            case PARADL_DATA: case PARADL_FILTER: case PARADL_CHANNEL: case PARADL_PD:
+            case PARADL_DATA: case PARADL_FILTER: case PARADL_CHANNEL: case PARADL_PD: case PARADL_DATA_LW:
                 ok = d[1] == 1 && d[2] == 1 && d[3] == 1; break;
             case PARADL_DF: ok = d[2] == 1 && d[3] == 1; break;
             case PARADL_SPATIAL: case PARADL_SPATIAL_AG: ok = d[0] == 1; break;
             default: break;
             }
             if (!ok) return fail(c, PARADL_EINVAL, "sub %d: dims tuple does not fit the family", i);
-            const int64_t deg = (fam == PARADL_DATA || fam == PARADL_DF || fam == PARADL_DS || fam == PARADL_PD) ? d[0] : 1;
+            const int64_t deg = (fam == PARADL_DATA || fam == PARADL_DF || fam == PARADL_DS || fam == PARADL_PD ||
+                                 fam == PARADL_DATA_LW)
+                                    ? d[0]
+                                    : 1;
             degmax = std::max(degmax, deg);
             pmax = std::max<int64_t>(pmax, (int64_t)d[0] * d[1] * d[2] * d[3]);
         }
@@ -745,6 +748,22 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 stride_digits(h, w);
             }
         }
+        if (fam == PARADL_DATA_LW) {
+            // per-layer Allreduce coefficients (c_l, s_l) per dims value, built in shared memory
+            // by every CTA (build_memo): [n_dims][weighted rows][2] doubles
+            const HostModel &hm = c->models[P.subs[q].model];
+            uint32_t lw = 0;
+            for (const auto &r : hm.rows) lw += r.w > 0;
+            const uint64_t n = (uint64_t)h.radix[D_DIMS] * lw * 2;
+            if (n * sizeof(double) > (64u << 10)) return fail(c, PARADL_EINVAL, "sub %d: data_lw table (dims x weighted layers) exceeds 64 KB", (int)q);
+            for (int i = 0; i < a.n_work; i++) {
+                WorkItem &w = a.work[i];
+                if (w.sub != (int32_t)q || w.memo_n) continue;
+                w.memo_n = (uint32_t)n;
+                w.memo_off = a.memo_bytes;
+                a.memo_bytes += (uint32_t)align16(n * sizeof(double));
+            }
+        }
         if (fam == PARADL_GPIPE) {
             // per-lane stage table (f, g, m, u per stage) of the GPipe schedule evaluation
             a.dtab_bytes = std::max<uint32_t>(a.dtab_bytes, kGpipeTabBytes);
@@ -779,6 +798,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     x.dtab_bytes = md == 1 ? dtab_bytes : 0;
                 } else if (fam_of[li] == PARADL_GPIPE) {
                     x.dtab_bytes = dtab_bytes;   // per-lane stage table
+                } else if (fam_of[li] == PARADL_DATA_LW) {
+                    x.memo_bytes = memo_bytes;   // per-layer Allreduce tables
                 }
                 if (first) {
                     L[li] = x;

@@ -367,6 +367,8 @@ struct Mid {
     bool pp_on;           // pipeline c (alpha + s beta) / layer-pure 2 (na alpha + s beta)
     double *gp;           // GPIPE: this lane's stage table f[i], g[i], m[i], u[i] at gp[(4i+k)*gps]
     int gps, gS, gns;     // table stride, segments S, stage count s
+    const double *lwt;    // DATA_LW: the work item's [n_dims][lwn][2] table of (c_l, s_l); row of
+    int lwn;              // the current dims value after compute_mid; lwn weighted layers
     // memoised divisions (same operands -> same IEEE result; recomputed when an operand changes)
     double R_memo, tau_memo;
     int64_t B_memo;
@@ -501,6 +503,16 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.ge2 = make_ar(H, p1, i2d(dW), div_i(dW, p1), to);  // Allreduce among leaders
         }
         m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p, 1);
+    } else if (FAM == PARADL_DATA_LW) {   // Data row, one Allreduce per weighted layer (Q37)
+        p = dm[0];
+        B = b * p;
+        m.comp = comp_term(B * M->FB, M->WU, p, 1, tau);
+        const int t = tier_of(H, p);
+        reason |= flag_tier(t);
+        m.pp_t = t;
+        m.lwt += (size_t)L.d[D_DIMS] * m.lwn * 2;
+        m.mem = mem_term(H, 2 * B * M->XY, M->W, M->BI, p, 1);
+        if (p > B) reason |= PARADL_R_SCALING;
     } else if (FAM == PARADL_SPATIAL_AG) {
         // Spatial on rows [0, Ls), Allgather of y_Ls, rows [Ls, G) replicated (Q35):
         // comp = ((B FB_pre / p) tau + (B FB_suf) tau) + WU tau; GE = AR(p, delta W);
@@ -793,6 +805,20 @@ __device__ __forceinline__ double gpipe_time(const Mid &m, double a, double be) 
     return t[0];
 }
 
+// DATA_LW gradient exchange: left fold over the weighted layers of c_l (alpha + s_l beta),
+// the per-message Allreduce of the table built by build_memo (ring or tree per message)
+__device__ __forceinline__ double lw_ge(const double *tab, int n, double a, double be) {
+    double ge = 0.0;
+    int j = 0;
+    for (; j + 2 <= n; j += 2) {   // two loads of (c, s) pairs per step; the fold stays in order
+        const double4 q = *reinterpret_cast<const double4 *>(tab + 2 * j);
+        ge = dadd(ge, dmul(q.x, dadd(a, dmul(q.y, be))));
+        ge = dadd(ge, dmul(q.z, dadd(a, dmul(q.w, be))));
+    }
+    if (j < n) ge = dadd(ge, dmul(tab[2 * j], dadd(a, dmul(tab[2 * j + 1], be))));
+    return ge;
+}
+
 struct Phases {
     double comp, ge, ag, ar, halo, p2p;
 };
@@ -804,6 +830,16 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
     double ge = 0.0, ag = 0.0, ar = 0.0, halo = 0.0, p2p = 0.0;
     double t = m.comp;
     if (!EXPLAIN && CHECK_TIER && (m.reason & PARADL_R_TIER)) return CUDART_INF;
+    if (FAM == PARADL_DATA_LW) {
+        ge = (EXPLAIN && m.pp_t < 0) ? CUDART_INF : lw_ge(m.lwt, m.lwn, arow[max(m.pp_t, 0)], brow[max(m.pp_t, 0)]);
+        t = dadd(t, ge);
+        if (EXPLAIN) {
+            ph->comp = m.comp;
+            ph->ge = ge;
+            ph->ag = ph->ar = ph->halo = ph->p2p = 0.0;
+        }
+        return t;
+    }
     if (FAM == PARADL_GPIPE) {
         t = (EXPLAIN && m.pp_t < 0) ? CUDART_INF : gpipe_time(m, arow[max(m.pp_t, 0)], brow[max(m.pp_t, 0)]);
         if (EXPLAIN) {
@@ -948,6 +984,7 @@ __device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const S
 template <int FAM>
 __device__ __forceinline__ double inner_fast(const Mid &m, const double *arow, const double *brow) {
     if constexpr (FAM == PARADL_GPIPE) return gpipe_time(m, arow[m.pp_t], brow[m.pp_t]);
+    if constexpr (FAM == PARADL_DATA_LW) return dadd(m.comp, lw_ge(m.lwt, m.lwn, arow[m.pp_t], brow[m.pp_t]));
     AlphaV a;
     SlotV v;
     alpha_vals<FAM>(m, arow, a);
@@ -1291,7 +1328,8 @@ __device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) 
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
 template <int FAM, bool DENSE>
 __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
-                                          uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, double *dtab) {
+                                          uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, double *dtab,
+                                          const double *memo) {
     const View v = make_view(smem, w.sub);
     const int lane = threadIdx.x & 31;
     const int cs = kThreads;
@@ -1309,7 +1347,8 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
     const uint32_t dB = 32u % nB, dA = 32u / nB;        // lane stride 32 inside the alpha/beta block
     // beta-slot caching (M = nB / 32) needs every lane of a step in the same 32-aligned beta
     // window, i.e. a 32-aligned range start (tile starts are lo + multiples of 32)
-    const bool slots = !GP && (nB == 32u || nB == 64u) && (w.lo & 31u) == 0;
+    constexpr bool LW = FAM == PARADL_DATA_LW;
+    const bool slots = !GP && !LW && (nB == 32u || nB == 64u) && (w.lo & 31u) == 0;
     const bool M2 = nB == 64u;
     const unsigned full = 0xffffffffu;
         const uint64_t u0 = w.lo + tile * TS;
@@ -1327,6 +1366,11 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
             m.gp = dtab + threadIdx.x;
             m.gps = kThreads;
         }
+        const double *lw_base = LW ? memo + w.memo_off / sizeof(double) : nullptr;
+        if (LW) {
+            m.lwt = lw_base;
+            m.lwn = (int)(w.memo_n / (2u * v.S->radix[D_DIMS]));
+        }
         // pipeline reduce tiles read the structure terms from the structure table
         const bool rec = REC && w.stab != nullptr;
         uint64_t sidx = 0;   // rec: the lane's structure index
@@ -1337,6 +1381,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 load_rec(w, sidx, m);
             } else {
                 if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+                if (LW) m.lwt = lw_base;
                 compute_mid<FAM>(v, L, st, m, w.halo);
                 if (GP) gpipe_fill(v, L, cuts, cs, m);
                 fastify(m);
@@ -1413,7 +1458,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 } else if (fb == full && slots) {
                     // every lane feasible and n_beta = 32*M: lane's beta values are fixed, so the
                     // s*beta products are formed once per run and reused for every alpha row
-                    if constexpr (!GP) {
+                    if constexpr (!GP && !LW) {
                         if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                         else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                     }
@@ -1549,6 +1594,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     } else {
                         if (PIPE && lvl >= D_PART)
                             stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
+                        if (LW) m.lwt = lw_base;
                         compute_mid<FAM>(v, L, st, m, w.halo);
                         if (GP) gpipe_fill(v, L, cuts, cs, m);
                         fastify(m);
@@ -2180,6 +2226,29 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
     }
     for (int wi = 0; wi < a.n_work; wi++) {
         const WorkItem &w = a.work[wi];
+        if (w.family == PARADL_DATA_LW && w.memo_n) {
+            // per dims value and weighted layer l (row order): the Allreduce of delta |w_l|
+            // over p PEs as c (alpha + s beta) -- make_ar's ring / tree choice per message
+            const View v = make_view(smem, w.sub);
+            const ModelHdr *M = v.M;
+            const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+            const int32_t *dmv = at<int32_t>(v.img, v.S->off_dims);
+            const uint32_t nD = v.S->radix[D_DIMS], G = (uint32_t)M->G, lwn = w.memo_n / (2u * nD);
+            double *tab = memo_base + w.memo_off / sizeof(double);
+            for (uint32_t e = threadIdx.x; e < nD * G; e += blockDim.x) {
+                const uint32_t iD = e / G, l = e - iD * G;
+                const int64_t wl = PW[l + 1] - PW[l];
+                if (wl <= 0) continue;
+                uint32_t j = 0;   // rank among the weighted rows
+                for (uint32_t q = 0; q < l; q++) j += PW[q + 1] > PW[q];
+                const int64_t p = dmv[4 * iD];
+                const ARt r = make_ar(v.H, p, i2d(v.H->delta * wl), div_i(v.H->delta * wl, p), 0);
+                double *o = tab + ((size_t)iD * lwn + j) * 2;
+                o[0] = r.on ? r.c : 0.0;
+                o[1] = r.on ? r.s : 0.0;
+            }
+            continue;
+        }
         if (w.mode == 0) continue;
         const View v = make_view(smem, w.sub);
         const SubHdr *S = v.S;
@@ -2320,7 +2389,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
     double *dtab = a.dtab_bytes ? reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes +
                                                              a.low_bytes)
                                 : nullptr;
-    if (BLK) build_memo(a, smem, memo, lowtab);
+    if (BLK || FAM == PARADL_DATA_LW) build_memo(a, smem, memo, lowtab);
 
     for (;;) {
         unsigned long long t = 0;
@@ -2341,7 +2410,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
                 tile_body_mask<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, lowtab + w.low_off);
         }
         else
-            tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt, dtab);
+            tile_body<FAM, DENSE>(a, w, T - w.tile_base, smem, cuts, tk, cnt, dtab, memo);
     }
 
     if (!DENSE) {
@@ -2564,13 +2633,33 @@ __device__ void explain_one(const View &v, const Lane &L, const uint16_t *cuts, 
     double gtab[4 * kGpMax];
     m.gp = gtab;
     m.gps = 1;
+    m.lwt = nullptr;
+    m.lwn = 0;
     compute_mid<FAM>(v, L, st, m);
     if (FAM == PARADL_GPIPE) gpipe_fill(v, L, cuts, 1, m);
     const int NT = v.H->n_tiers;
     const double *arow = at<double>(v.img, v.S->off_alpha) + (size_t)L.d[D_ALPHA] * NT;
     const double *brow = at<double>(v.img, v.S->off_beta) + (size_t)L.d[D_BETA] * NT;
     Phases ph;
-    const double t = inner<FAM, true>(m, arow, brow, &ph);
+    double t;
+    if constexpr (FAM == PARADL_DATA_LW) {
+        // the per-layer Allreduce fold of lw_ge, row by row (no shared table here)
+        const int64_t *PW = at<int64_t>(v.mb, v.M->off_pw);
+        const int64_t p = m.p;
+        double ge = 0.0;
+        if (m.pp_t < 0) ge = CUDART_INF;
+        else
+            for (int l = 0; l < v.M->G; l++) {
+                const int64_t wl = PW[l + 1] - PW[l];
+                if (wl <= 0) continue;
+                const ARt r = make_ar(v.H, p, i2d(v.H->delta * wl), div_i(v.H->delta * wl, p), 0);
+                ge = dadd(ge, dmul(r.on ? r.c : 0.0, dadd(arow[m.pp_t], dmul(r.on ? r.s : 0.0, brow[m.pp_t]))));
+            }
+        ph = Phases{m.comp, ge, 0.0, 0.0, 0.0, 0.0};
+        t = dadd(m.comp, ge);
+    } else {
+        t = inner<FAM, true>(m, arow, brow, &ph);
+    }
     pr->t_comp = ph.comp;
     pr->t_ge = ph.ge;
     pr->t_fb_ag = ph.ag;
@@ -2646,6 +2735,7 @@ __global__ void explain_kernel(const uint8_t *img, int32_t sub, uint64_t local, 
     case PARADL_PD: explain_one<PARADL_PD>(v, L, cuts, cfg, pr); break;
     case PARADL_SPATIAL_AG: explain_one<PARADL_SPATIAL_AG>(v, L, cuts, cfg, pr); break;
     case PARADL_GPIPE: explain_one<PARADL_GPIPE>(v, L, cuts, cfg, pr); break;
+    case PARADL_DATA_LW: explain_one<PARADL_DATA_LW>(v, L, cuts, cfg, pr); break;
     default: break;
     }
 }
@@ -2903,6 +2993,7 @@ static void *sweep_fn(int family, bool dense, int blk) {
         PARADL_CASE(PARADL_PD)
         PARADL_CASE(PARADL_SPATIAL_AG)
         PARADL_CASE(PARADL_GPIPE)
+        PARADL_CASE(PARADL_DATA_LW)
     default: return nullptr;
     }
 #undef PARADL_CASE

@@ -226,4 +226,16 @@ def next_spatial_ag(n_alpha=64, n_beta=64) -> Sweep:
     return Sweep(ms, sys, subs, "next_spatial_ag")
 
 
-NEXT = {"gpipe": next_gpipe, "spatial_ag": next_spatial_ag}
+def next_data_lw(n_alpha=256, n_beta=256) -> Sweep:
+    """Per-layer gradient messages with per-message ring / tree dispatch (family DATA_LW,
+    P:552, Q37): ResNet-50, ResNet-152 and VGG16, p in 2^0..2^10, b in
+    2^0..2^8, a 256 x 256 alpha/beta grid; messages below 1 MiB use the 4-chunk tree form."""
+    ms = [M.resnet(50), M.resnet(152), M.vgg16()]
+    sys = two_tier_system(flops_per_s=37e12, hbm_bytes=80 * GiB, tree_threshold=float(1 << 20), tree_chunks=4)
+    A, B = ab_grid(np.logspace(-7, -4, n_alpha), 1.0 / np.logspace(9, 12, n_beta))
+    subs = [SubSweep(DATA_LW, model=mi, dims=[(p, 1, 1, 1) for p in pow2(0, 10)], b=pow2(0, 8), alpha=A, beta=B)
+            for mi in range(3)]
+    return Sweep(ms, sys, subs, "next_data_lw")
+
+
+NEXT = {"gpipe": next_gpipe, "spatial_ag": next_spatial_ag, "data_lw": next_data_lw}
