@@ -695,6 +695,10 @@ __device__ void gpipe_fill(const View &v, const Lane &L, const uint16_t *cuts, i
 #define PARADL_GP_QUAD 2
 #endif
 constexpr uint32_t kGpQuad = PARADL_GP_QUAD;   // GPipe configurations per schedule call
+#ifndef PARADL_LW_QUAD
+#define PARADL_LW_QUAD 4
+#endif
+constexpr uint32_t kLwQuad = PARADL_LW_QUAD;   // DATA_LW configurations per interleaved fold
 
 // max of two non-negative, non-NaN doubles as one compare + two 32-bit selects (fmax adds
 // NaN handling: a third ALU instruction per max on sm_100a, which has no DMNMX)
@@ -803,6 +807,18 @@ __device__ __forceinline__ double gpipe_time(const Mid &m, double a, double be) 
     double t[1];
     gpipe_eval<1>(m.gp, m.gps, m.gns, m.gS, &a, &be, t);
     return t[0];
+}
+
+// NC interleaved folds (independent configurations, same table): ILP for the serial chain
+template <int NC>
+__device__ __forceinline__ void lw_ge_n(const double *tab, int n, const double *a, const double *be, double *ge) {
+#pragma unroll
+    for (int c = 0; c < NC; c++) ge[c] = 0.0;
+    for (int j = 0; j < n; j++) {
+        const double2 q = *reinterpret_cast<const double2 *>(tab + 2 * j);
+#pragma unroll
+        for (int c = 0; c < NC; c++) ge[c] = dadd(ge[c], dmul(q.x, dadd(a[c], dmul(q.y, be[c]))));
+    }
 }
 
 // DATA_LW gradient exchange: left fold over the weighted layers of c_l (alpha + s_l beta),
@@ -1462,10 +1478,11 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                         if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                         else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                     }
-                } else if (GP && fb == full) {
-                    // GPipe schedule: two (alpha, beta) configurations per call, interleaved chains
+                } else if ((GP || LW) && fb == full) {
+                    // GPipe schedule / per-layer folds: Q (alpha, beta) configurations per call,
+                    // interleaved dependency chains
                     const int ts = m.pp_t;
-                    constexpr uint32_t Q = kGpQuad;
+                    constexpr uint32_t Q = LW ? kLwQuad : kGpQuad;
                     uint32_t r = 0;
                     for (; r + Q <= run; r += Q) {
                         double av[Q], bv[Q], kv[Q];
@@ -1480,7 +1497,13 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                                 alpha_i++;
                             }
                         }
-                        gpipe_eval<Q>(m.gp, m.gps, m.gns, m.gS, av, bv, kv);
+                        if constexpr (LW) {
+                            lw_ge_n<(int)Q>(m.lwt, m.lwn, av, bv, kv);
+#pragma unroll
+                            for (uint32_t c = 0; c < Q; c++) kv[c] = dadd(m.comp, kv[c]);
+                        } else {
+                            gpipe_eval<Q>(m.gp, m.gps, m.gns, m.gS, av, bv, kv);
+                        }
                         bool any = false;
 #pragma unroll
                         for (uint32_t c = 0; c < Q; c++) {
@@ -1494,8 +1517,8 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     }
 #pragma unroll 1
                     for (; r < run; r++) {
-                        const double key = dmul(gpipe_time(m, alpha_tab[(size_t)alpha_i * NT + ts],
-                                                           beta_tab[(size_t)beta_i * NT + ts]),
+                        const double key = dmul(inner_fast<FAM>(m, alpha_tab + (size_t)alpha_i * NT,
+                                                                beta_tab + (size_t)beta_i * NT),
                                                 m.I);
                         if (__any_sync(full, key <= tk.adm)) tk.offer(true, key, g0 + lane + 32ull * (j + r));
                         beta_i += dB;
