@@ -316,7 +316,7 @@ def ours(args):
     # dominant kernel: the largest sub-sweep of the workload (cfg2: the pipeline family)
     sizes = []
     for i, sb in enumerate(sweep.subs):
-        sizes.append((P.Spec([sb], [spec.c.sub[i].model_id]), i))
+        sizes.append((sub_spec(P, spec, sweep, i), i))
     sizes = [(ctx.sweep_size(sp), i, sp) for sp, i in sizes]
     ctx.set_system(sweep.system)
     dom = max(sizes, key=lambda t: t[0])[1:] if sizes else None
@@ -500,8 +500,8 @@ def next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak):
             ops = 0.0
             for si, sb in enumerate(sw.subs):
                 lw = sum(1 for r in sw.models[sb.model].layers if r.w > 0)
-                sub_spec = P.Spec([sb], [spec.c.sub[si].model_id])
-                _, c = ctx.topk(sub_spec, 1, 0, ctx.sweep_size(sub_spec))
+                ss = sub_spec(P, spec, sw, si)
+                _, c = ctx.topk(ss, 1, 0, ctx.sweep_size(ss))
                 ops += c * (4.0 * lw + 2.0)
             ctx.prepare(sw)
             opc = ops / max(1, n_feas)
@@ -517,6 +517,12 @@ def next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak):
                                   "unit": "T fp64-pipe inst/s", "frac": ach / (fp64_peak / 1e12),
                                   "fp64_inst_per_config": opc}}
     return out
+
+
+def sub_spec(P, spec, sweep, i):
+    """C spec of sub-sweep i alone (model ids as loaded for the whole sweep)."""
+    mids = {sb.model: spec.c.sub[j].model_id for j, sb in enumerate(sweep.subs)}
+    return P.Spec([sweep.subs[i]], mids)
 
 
 def spec_model_id(ctx, spec, sub_index):
