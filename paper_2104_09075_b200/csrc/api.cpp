@@ -902,7 +902,10 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 // tile (structure terms are computed once per block), 32..131072 configs per tile
                 const SubHdr &h = P.subs[w.sub].hdr;
                 const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
-                uint64_t steps = std::max<uint64_t>(range / n_shards / (32ull * warps * 8ull), (nAB + 31) / 32);
+                // families whose per-configuration work dwarfs the structure terms (a schedule,
+                // a per-layer fold) split alpha/beta blocks across warps instead
+                const bool heavy = w.family == PARADL_GPIPE || w.family == PARADL_DATA_LW;
+                uint64_t steps = std::max<uint64_t>(range / n_shards / (32ull * warps * 8ull), heavy ? 4 : (nAB + 31) / 32);
                 steps = std::max<uint64_t>(1, std::min<uint64_t>(steps, 4096));
                 w.steps = (uint32_t)steps;
                 w.n_tiles = (range + 32ull * steps - 1) / (32ull * steps);
