@@ -1,0 +1,96 @@
+"""Empirical parametrization on CPU: the alpha/beta fit inverts
+the ring Allreduce form exactly, the gloo world-2 measurement path runs end to end, and
+measured per-layer times become a layer table the oracle accepts (FW_l = measured)."""
+from __future__ import annotations
+
+import os
+import random
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import toys
+from workloads import calibrate as CAL
+from workloads import models as M
+from workloads import sweeps as W
+
+
+def test_fit_recovers_ring_parameters():
+    rng = random.Random(5)
+    for _ in range(20):
+        p = rng.choice([2, 4, 8, 64])
+        a, b = rng.uniform(1e-6, 5e-5), 1.0 / rng.uniform(1e9, 9e11)
+        sizes = [1 << e for e in range(10, 29, 2)]
+        t = [2 * (p - 1) * (a + m / p * b) for m in sizes]
+        fa, fb, rms = CAL.fit_allreduce(p, sizes, t)
+        assert abs(fa - a) <= 1e-9 * a and abs(fb - b) <= 1e-9 * b and rms < 1e-12
+        noisy = [v * (1 + rng.uniform(-0.02, 0.02)) for v in t]
+        fa, fb, rms = CAL.fit_allreduce(p, sizes, noisy)
+        assert abs(fa - a) <= 0.1 * a and abs(fb - b) <= 0.1 * b and rms < 0.05
+
+
+def test_fit_rejects_single_pe():
+    with pytest.raises(ValueError):
+        CAL.fit_allreduce(1, [1, 2], [1.0, 2.0])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, ws, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        tier = CAL.calibrate_tier([1 << 12, 1 << 16, 1 << 20], reps=3, device=torch.device("cpu"))
+        if rank == 0:
+            q.put(tier)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_calibration():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    tier = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert tier["p"] == 2 and len(tier["times_s"]) == 3
+    assert all(t > 0 for t in tier["times_s"])
+    assert tier["alpha_s"] >= 0 and tier["beta_s_per_B"] > 0
+    s = CAL.system_from_tiers([tier], flops_per_s=1e12, hbm_bytes=16e9)
+    assert s.tiers[0].max_pes == 2
+
+
+def test_measured_layer_table(oracle_mod):
+    """Per-layer times on CPU for a small conv / FC model; the empirical table gives the
+    oracle's serial compute = sum of the measured per-sample times x b (+ WU)."""
+    rows = [M.make_conv("c1", 3, 8, (16, 16), 3, pad=1), M.make_conv("c2", 8, 8, (16, 16), 3, stride=2, pad=1),
+            M.make_fc("fc", 8 * 8 * 8, 10, (1, 1))]
+    m = M.Model("tiny", rows, 100, default_Ls=2)
+    times = CAL.time_layers(m, b=4, reps=2, warmup=1, device=torch.device("cpu"))
+    assert times[0] is not None and times[2] is not None
+    R = 1e12
+    em = CAL.empirical_model(m, times, R)
+    for r, t in zip(em.layers, times):
+        if t is not None:
+            assert abs(r.fw / R - t[0]) <= 1e-12 + 1e-9 * t[0]
+    sysm = W.two_tier_system(flops_per_s=R)
+    sw = W.Sweep([em], sysm, [W.SubSweep(W.SERIAL, b=[4])], "emp")
+    o = oracle_mod.OracleSweep(sw)
+    pr = o.explain(0)
+    want = 4 * sum((r.fw + r.bw) for r in em.layers) / R + sum(r.wu for r in em.layers) / R
+    assert abs(pr.t_comp - want) <= 1e-12 * want
