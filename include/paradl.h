@@ -131,7 +131,8 @@ typedef struct {
     double phi_df;              /* >= 1: contention on the df inter-group Allreduce */
     double tree_threshold_B;    /* >= 0: Allreduce messages below it use the tree form; 0 = ring only */
     int32_t tree_chunks;        /* k >= 1 of the tree form */
-    int32_t reserved;
+    int32_t filter_rs;          /* 0: filter/channel/df backward dL/dx exchange is an Allreduce (Table 2);
+                                   1: a Reduce-Scatter, (p-1)(alpha + (m/p) beta) (P:355 footnote; Q38) */
 } paradl_system;
 
 /* Base system: default alpha/beta per tier, R, capacity (sweeps may override per radix). */

@@ -470,7 +470,7 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (p > 1) {
             ag = t < 0 ? INFINITY
                        : (double)(p - 1) * ((double)s.NC * c->alpha[t] + ((double)BdYC / (double)p) * c->beta[t]);
-            ar = 2.0 * ag;
+            ar = (sys->filter_rs ? 1.0 : 2.0) * ag;   /* Reduce-Scatter = one Allgather's cost (P:355 fn) */
         }
         mem = mem_term(sys, twoBXY, s.W, s.BI, 1, p);
         if (c->family == OR_FILTER ? (p > s.Fmin) : (p > s.Cmin2)) reason |= OR_R_SCALING;
@@ -490,7 +490,7 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (p2 > 1) {
             ag = ti < 0 ? INFINITY
                         : (double)(p2 - 1) * ((double)s.NC * c->alpha[ti] + ((double)BdYC / (double)p) * c->beta[ti]);
-            ar = 2.0 * ag;
+            ar = (sys->filter_rs ? 1.0 : 2.0) * ag;   /* Reduce-Scatter = one Allgather's cost (P:355 fn) */
         }
         /* 2(p1-1)(alpha + (sum|w|/p) delta beta), contention phi on the shared link (Q30) */
         double phi = p2 > 1 ? sys->phi_df : 1.0;
@@ -790,7 +790,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
             sum += c->alpha[t] + ((double)B * (double)m->rows[l].y / (double)p) * dl * c->beta[t];
         }
         o->t_fb_ag = (double)(pg - 1) * sum;
-        o->t_fb_ar = 2.0 * (double)(pg - 1) * sum;
+        o->t_fb_ar = (sys->filter_rs ? 1.0 : 2.0) * (double)(pg - 1) * sum;
     }
     if ((fam == OR_SPATIAL || fam == OR_DS) && o->t_halo != 0.0 && isfinite(o->t_halo)) {
         int32_t split[3] = {d[1], d[2], d[3]};

@@ -52,7 +52,7 @@ typedef struct {
     int32_t n_tiers, delta;
     or_tier tiers[OR_MAX_TIERS];
     double flops_per_s, hbm_bytes, gamma, phi_df, tree_threshold;
-    int32_t tree_chunks, pad_;
+    int32_t tree_chunks, filter_rs;   /* filter_rs: backward dL/dx exchange as Reduce-Scatter (P:355 fn) */
 } or_system;
 
 typedef struct {

@@ -54,7 +54,7 @@ class System(C.Structure):
     _fields_ = [("n_tiers", C.c_int32), ("delta", C.c_int32), ("tiers", Tier * MAX_TIERS),
                 ("flops_per_s", C.c_double), ("hbm_bytes", C.c_double), ("gamma", C.c_double),
                 ("phi_df", C.c_double), ("tree_threshold", C.c_double),
-                ("tree_chunks", C.c_int32), ("pad_", C.c_int32)]
+                ("tree_chunks", C.c_int32), ("filter_rs", C.c_int32)]
 
 
 class Sub(C.Structure):
@@ -175,6 +175,7 @@ class OracleSweep:
         self.system.phi_df = s.phi_df
         self.system.tree_threshold = s.tree_threshold
         self.system.tree_chunks = s.tree_chunks
+        self.system.filter_rs = s.filter_rs
         subs = (Sub * max(1, len(sweep.subs)))()
         for i, sb in enumerate(sweep.subs):
             x = subs[i]

@@ -70,6 +70,7 @@ def make_system(s) -> A.System:
     S.phi_df = s.phi_df
     S.tree_threshold_B = s.tree_threshold
     S.tree_chunks = s.tree_chunks
+    S.filter_rs = s.filter_rs
     return S
 
 

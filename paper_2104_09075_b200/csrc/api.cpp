@@ -270,6 +270,7 @@ extern "C" paradl_status paradl_set_system(paradl_ctx *c, const paradl_system *s
     if (!(std::isfinite(s->phi_df) && s->phi_df >= 1.0)) return fail(c, PARADL_EINVAL, "phi_df must be >= 1");
     if (!(std::isfinite(s->tree_threshold_B) && s->tree_threshold_B >= 0.0) || s->tree_chunks < 1)
         return fail(c, PARADL_EINVAL, "tree_threshold >= 0 and tree_chunks >= 1 required");
+    if (s->filter_rs != 0 && s->filter_rs != 1) return fail(c, PARADL_EINVAL, "filter_rs must be 0 or 1");
     c->sys = *s;
     c->have_system = true;
     c->img_epoch = ~0ull;
@@ -506,6 +507,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
     H.n_tiers = NT;
     H.delta = sy.delta;
     H.tree_chunks = sy.tree_chunks;
+    H.ar_mult = sy.filter_rs ? 1.0 : 2.0;
     H.gamma = sy.gamma;
     H.phi_df = sy.phi_df;
     H.tree_thr = sy.tree_threshold_B;

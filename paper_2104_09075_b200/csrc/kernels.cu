@@ -356,7 +356,7 @@ struct Mid {
     int64_t B, p;
     ARt ge, ge2;          // GE (data/spatial/df/pd), ds: reduce-to-leader (ge) + leaders (ge2)
     double phi;           // df inter-group contention multiplier on beta
-    double ag_c, ag_na, ag_s;
+    double ag_c, ag_na, ag_s, ar_mult;
     int ag_t;
     bool ag_on;           // filter/channel/df Allgather phase (Allreduce = 2x)
     double h_na, h_s;
@@ -459,6 +459,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
     const int64_t dW = delta * M->W;
     uint32_t reason = 0;
     m.ge.on = m.ge2.on = m.ag_on = m.h_on = m.pp_on = false;
+    m.ar_mult = H->ar_mult;
     m.phi = 1.0;
     int64_t B = b, p = 1;
     if (FAM == PARADL_SERIAL) {   // Table 2 Serial row
@@ -891,7 +892,7 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
         if (m.ag_on) {
             if (EXPLAIN && m.ag_t < 0) ag = CUDART_INF;
             else ag = dmul(m.ag_c, dadd(dmul(m.ag_na, arow[m.ag_t]), dmul(m.ag_s, brow[m.ag_t])));
-            ar = dmul(2.0, ag);
+            ar = dmul(m.ar_mult, ag);
             t = dadd(dadd(t, ag), ar);
         }
     }
@@ -989,7 +990,7 @@ __device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const S
     if (FAM == PARADL_DS) t = dadd(t, dadd(dmul(m.ge.c, dadd(a.ge, v.ge)), dmul(m.ge2.c, dadd(a.ge2, v.ge2))));
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) {
         const double ag = dmul(m.ag_c, dadd(a.ag, v.ag));
-        t = dadd(dadd(t, ag), dmul(2.0, ag));
+        t = dadd(dadd(t, ag), dmul(m.ar_mult, ag));
     }
     if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) t = dadd(t, dmul(2.0, dadd(a.h, v.h)));
     if (FAM == PARADL_PIPELINE || FAM == PARADL_PD) t = dadd(t, dmul(m.pp_c, dadd(a.pp, v.pp)));

@@ -56,6 +56,8 @@ struct ImgHdr {
     int32_t n_sub, n_models, n_tiers;
     int32_t delta, tree_chunks;
     double gamma, phi_df, tree_thr;
+    double ar_mult;                    // filter/channel/df FB-AR = ar_mult x FB-AG: 2 (Allreduce), 1 (Reduce-Scatter)
+    double pad_hdr;
     int64_t max_pes[PARADL_MAX_TIERS];
     uint32_t model_off[kMaxModelsPerSweep];
     uint32_t sub_off[kMaxSub];

@@ -217,7 +217,7 @@ def exact(sweep, cfg):
         t = tier(p)
         if p > 1:
             ag = inf if t is None else (p - 1) * sum(A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm)
-            ar = inf if t is None else 2 * (p - 1) * sum(A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm)
+            ar = inf if t is None else (1 if sys.filter_rs else 2) * (p - 1) * sum(A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm)
         mem = mem_row(B, 1, p)
         if fam == W.FILTER:
             lim = min((L[l].F for l in comm_rows), default=None)
@@ -233,7 +233,7 @@ def exact(sweep, cfg):
         ti, to = tier(p2), tier(p)
         if p2 > 1:
             ag = inf if ti is None else (p2 - 1) * sum(A[ti] + Fr(B * L[l].y, p) * dl * Bt[ti] for l in Cm)
-            ar = inf if ti is None else 2 * (p2 - 1) * sum(A[ti] + Fr(B * L[l].y, p) * dl * Bt[ti] for l in Cm)
+            ar = inf if ti is None else (1 if sys.filter_rs else 2) * (p2 - 1) * sum(A[ti] + Fr(B * L[l].y, p) * dl * Bt[ti] for l in Cm)
         phi = Fr(sys.phi_df) if p2 > 1 else Fr(1)
         if to is None:
             ge = inf if p1 > 1 else Fr(0)

@@ -476,6 +476,30 @@ def test_data_lw_per_message_dispatch(oracle_mod):
     assert _rel(lw.t_ge, tree_small + ring_large) <= 1e-15
 
 
+# ------------------------------------------------------------ filter Reduce-Scatter variant (Q38)
+def test_filter_reduce_scatter_variant(oracle_mod):
+    """P:355 footnote: layer l-1 needs only its partition of dL/dx, so the backward exchange
+    can be a Reduce-Scatter: (p-1) steps of the per-PE segment (the ring's first half,
+    P:553-556), i.e. one Allgather's cost instead of the Allreduce's two.  With filter_rs
+    the FB-AR phase equals FB-AG bit for bit; filter / channel / df all switch."""
+    m = corpus.random_model(3)
+    for fam, dims in ((W.FILTER, (4, 1, 1, 1)), (W.CHANNEL, (2, 1, 1, 1)), (W.DF, (2, 2, 1, 1))):
+        for rs in (0, 1):
+            sysm = toys.system(delta=4, alpha=1e-6, beta=1e-9)
+            sysm.filter_rs = rs
+            pr = _one(oracle_mod, m, sysm, W.SubSweep(fam, b=[2], dims=[dims]))
+            if pr.t_fb_ag == 0.0:
+                continue
+            if rs:
+                assert pr.t_fb_ar == pr.t_fb_ag
+            else:
+                assert pr.t_fb_ar == 2.0 * pr.t_fb_ag
+    # the Reduce-Scatter cost is the ring simulation's reduce-scatter half
+    p, seg = 4, Fr(1000)
+    full, _ = brute.ring_allreduce_sim(p, seg * p, Fr(1e-6), Fr(1e-9))
+    assert full / 2 == brute.ring_allgather_sim(p, seg, Fr(1e-6), Fr(1e-9))
+
+
 # ------------------------------------------------------------ memory
 @pytest.mark.parametrize("seed", range(25))
 def test_memory_rows_equal_buffer_enumeration(oracle_mod, seed):

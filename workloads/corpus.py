@@ -60,7 +60,8 @@ def random_system(seed: int) -> W.System:
                     gamma=rng.choice([1.0, 0.5, 0.37]),
                     phi_df=rng.choice([1.0, 2.0, 3.0]),
                     tree_threshold=rng.choice([0.0, 0.0, 4096.0, 1e6]),
-                    tree_chunks=rng.choice([1, 2, 4]))
+                    tree_chunks=rng.choice([1, 2, 4]),
+                    filter_rs=rng.choice([0, 1]))
 
 
 def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:

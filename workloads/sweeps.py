@@ -48,6 +48,7 @@ class System:
     phi_df: float = 2.0
     tree_threshold: float = 0.0     # bytes; 0 => ring everywhere (Table 2 literal)
     tree_chunks: int = 1
+    filter_rs: int = 0              # 1: filter/channel backward exchange as Reduce-Scatter (P:355 fn)
 
 
 @dataclass
