@@ -23,6 +23,9 @@
 namespace paradl {
 
 // tuning knobs (experiments build variants with -D; defaults are the measured best)
+#ifndef PARADL_RELAXED_BOUND
+#define PARADL_RELAXED_BOUND 1
+#endif
 #ifndef PARADL_MINB
 #define PARADL_MINB 2
 #endif
@@ -1038,11 +1041,20 @@ struct WarpTopK {
     // adopt the shared bound loaded at the previous call and issue the next load, so the
     // global-memory latency overlaps the work in between (whole warp; broadcast load)
     // (blocking while this warp has no bound at all, e.g. short-lived warps of small launches)
+    __device__ __forceinline__ static unsigned long long load_bound(const unsigned long long *p) {
+#if PARADL_RELAXED_BOUND
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+        return v;
+#else
+        return *(volatile const unsigned long long *)p;
+#endif
+    }
     __device__ __forceinline__ void refresh() {
         if (!gbound) return;
         unsigned long long g = gnext;
-        if (adm == CUDART_INF) g = *(volatile unsigned long long *)gbound;
-        gnext = *(volatile unsigned long long *)gbound;
+        if (adm == CUDART_INF) g = load_bound(gbound);
+        gnext = load_bound(gbound);
         if (g != ~0ull) adm = dmin_nn(adm, dmin_nn(thk, __longlong_as_double((long long)g)));
     }
     // after thk changed: tighten adm and publish a full list's threshold
