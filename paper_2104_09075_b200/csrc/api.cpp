@@ -925,8 +925,13 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * total_ctas * k));
     if (!dense) CUDA_TRY(c, c->nvalid.ensure(sizeof(uint32_t) * total_ctas));
     unsigned long long *ctr = (unsigned long long *)c->counters.p;
-    CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
-    CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
+    if (!sjobs.empty()) {   // the first structure-table launch zeroes them (it precedes every sweep)
+        sjobs[0].ctr = ctr;
+        sjobs[0].n_ctr = (int32_t)(nl + 1);
+    } else {
+        CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
+        CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
+    }
 
     if (halo_entries) {
         CUDA_TRY(c, launch_halo_tables(hj, st));

@@ -2920,6 +2920,8 @@ __global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, u
     // staged into shared memory first (one TMA bulk copy, as in the sweep kernels)
     extern __shared__ __align__(128) uint8_t simg[];
     __shared__ uint64_t mbar;
+    if (job.ctr && blockIdx.x == 0)   // replaces two memsets ahead of the sweep launches
+        for (int i = threadIdx.x; i <= job.n_ctr; i += blockDim.x) job.ctr[i] = i < job.n_ctr ? 0ull : ~0ull;
     stage_image(simg, img, img_bytes, &mbar);
     const View v = make_view(simg, job.sub);
     const SubHdr *S = v.S;

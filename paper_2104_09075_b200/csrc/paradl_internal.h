@@ -120,6 +120,8 @@ struct StructJob {
     int32_t sub, pad;
     uint64_t s_lo, n;              // structures [s_lo, s_lo + n) of sub-sweep `sub`
     PipeRec *out;
+    unsigned long long *ctr;       // non-null: zero ctr[0, n_ctr) and set ctr[n_ctr] = ~0 (the
+    int32_t n_ctr, pad2;           // sweep's tile counters, count and admission bound) first
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).
