@@ -1211,9 +1211,11 @@ __device__ __forceinline__ void WarpTopK::offer(bool valid, double key, uint64_t
 // lane step r visits beta = base + 32*slot, slot cycling 0..M-1, alpha advancing after
 // slot M-1.  idx0 = global index of the lane's first configuration of the run.  On exit
 // (alpha_i, beta_i) is the lane's last evaluated configuration.
-template <int FAM, int M>
+template <int FAM, int M, int NTC = 0>
 __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const double *alpha_tab, const double *beta_tab,
-                                          int NT, uint32_t &alpha_i, uint32_t &beta_i, uint32_t run, uint64_t idx0) {
+                                          int NT_, uint32_t &alpha_i, uint32_t &beta_i, uint32_t run, uint64_t idx0) {
+    // NTC > 0: the tier count is a compile-time constant (alpha rows at immediate offsets)
+    const int NT = NTC > 0 ? NTC : NT_;
     const unsigned full = 0xffffffffu;
     const uint32_t base = beta_i & 31u;
     SlotV sv[M];
@@ -1488,8 +1490,12 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     // every lane feasible and n_beta = 32*M: lane's beta values are fixed, so the
                     // s*beta products are formed once per run and reused for every alpha row
                     if constexpr (!GP && !LW) {
-                        if (M2) run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
-                        else run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                        if (M2 && NT == 2)
+                            run_slots<FAM, 2, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                        else if (M2)
+                            run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                        else
+                            run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                     }
                 } else if ((GP || LW) && fb == full) {
                     // GPipe schedule / per-layer folds: Q (alpha, beta) configurations per call,
