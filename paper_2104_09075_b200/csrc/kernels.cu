@@ -2554,65 +2554,85 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
         const unsigned long long g = *gbound;
         if (g != ~0ull) hit_min(bk, bi, __longlong_as_double((long long)g), ~0ull);
     }
-    // 2. candidates <= bound: one thread per entry (independent, coalesced loads; a per-list
-    //    walk would chain one global-memory latency per entry)
-    const int64_t n_ent = n_lists * (int64_t)k;
-    if (nvalid && n_lists <= kMergeLists) {
-        // pruned lists: exclusive prefix of the valid counts (warp 0, lane-chunked scan),
-        // then one thread per valid entry (independent loads, one memory latency)
-        for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) s_pre[l + 1] = nvalid[l];
-        __syncthreads();
-        if (warp == 0) {
-            const int nl = (int)n_lists, per = (nl + 31) / 32, b0 = min(nl, lane * per), b1 = min(nl, b0 + per);
-            uint32_t sum = 0;
-            for (int l = b0; l < b1; l++) sum += s_pre[l + 1];
-            uint32_t inc = sum;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(full, inc, o);
-                if (lane >= o) inc += v;
+    // 2. candidates <= bound: one thread per entry (independent, coalesced loads).  Massive
+    //    ties at the bound can overflow the candidate buffer: then the k-th smallest of the
+    //    buffered candidates (real entries, so still a valid bound, now with an index that
+    //    splits the ties) replaces the bound and the collection is repeated.
+    for (int round = 0;; round++) {
+        const int64_t n_ent = n_lists * (int64_t)k;
+        if (nvalid && n_lists <= kMergeLists) {
+            // pruned lists: exclusive prefix of the valid counts (warp 0, lane-chunked scan),
+            // then one thread per valid entry (independent loads, one memory latency)
+            for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) s_pre[l + 1] = nvalid[l];
+            __syncthreads();
+            if (warp == 0) {
+                const int nl = (int)n_lists, per = (nl + 31) / 32, b0 = min(nl, lane * per), b1 = min(nl, b0 + per);
+                uint32_t sum = 0;
+                for (int l = b0; l < b1; l++) sum += s_pre[l + 1];
+                uint32_t inc = sum;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(full, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                uint32_t run = inc - sum;
+                for (int l = b0; l < b1; l++) {
+                    const uint32_t v = s_pre[l + 1];
+                    s_pre[l] = run;
+                    run += v;
+                }
+                if (lane == 31) s_pre[nl] = inc;
             }
-            uint32_t run = inc - sum;
-            for (int l = b0; l < b1; l++) {
-                const uint32_t v = s_pre[l + 1];
-                s_pre[l] = run;
-                run += v;
+            __syncthreads();
+            const uint32_t V = s_pre[n_lists];
+            for (uint32_t e = threadIdx.x; e < V; e += blockDim.x) {
+                int lo = 0, hi = (int)n_lists;   // last list with s_pre[l] <= e
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_pre[mid] <= e) lo = mid;
+                    else hi = mid;
+                }
+                const paradl_hit h = lists[(int64_t)lo * lstride + (e - s_pre[lo])];
+                if (hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
+                const int pos = atomicAdd(&s_nc, 1);
+                if (pos < kMergeCand) cand[pos] = h;
             }
-            if (lane == 31) s_pre[nl] = inc;
-        }
-        __syncthreads();
-        const uint32_t V = s_pre[n_lists];
-        for (uint32_t e = threadIdx.x; e < V; e += blockDim.x) {
-            int lo = 0, hi = (int)n_lists;   // last list with s_pre[l] <= e
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (s_pre[mid] <= e) lo = mid;
-                else hi = mid;
+        } else if (nvalid) {
+            for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
+                const int nv = (int)nvalid[l];
+                for (int j = 0; j < nv; j++) {
+                    const paradl_hit h = lists[l * lstride + j];
+                    if (hit_less(bk, bi, h.key_epoch_s, h.idx)) break;   // sorted: the rest is larger
+                    const int pos = atomicAdd(&s_nc, 1);
+                    if (pos < kMergeCand) cand[pos] = h;
+                }
             }
-            const paradl_hit h = lists[(int64_t)lo * lstride + (e - s_pre[lo])];
-            if (hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
-            const int pos = atomicAdd(&s_nc, 1);
-            if (pos < kMergeCand) cand[pos] = h;
-        }
-    } else if (nvalid) {
-        for (int64_t l = threadIdx.x; l < n_lists; l += blockDim.x) {
-            const int nv = (int)nvalid[l];
-            for (int j = 0; j < nv; j++) {
+        } else {
+            for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
+                const int64_t l = e / k, j = e - l * k;
                 const paradl_hit h = lists[l * lstride + j];
-                if (hit_less(bk, bi, h.key_epoch_s, h.idx)) break;   // sorted: the rest is larger
+                if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
                 const int pos = atomicAdd(&s_nc, 1);
                 if (pos < kMergeCand) cand[pos] = h;
             }
         }
-    } else {
-        for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
-            const int64_t l = e / k, j = e - l * k;
-            const paradl_hit h = lists[l * lstride + j];
-            if (h.idx == ~0ull || hit_less(bk, bi, h.key_epoch_s, h.idx)) continue;
-            const int pos = atomicAdd(&s_nc, 1);
-            if (pos < kMergeCand) cand[pos] = h;
+        __syncthreads();
+        if (s_nc <= kMergeCand || round == 8) break;
+        // tighter bound: the candidate of rank k-1 among the buffered ones
+        for (int i = threadIdx.x; i < kMergeCand; i += blockDim.x) {
+            const paradl_hit h = cand[i];
+            int r = 0;
+            for (int j = 0; j < kMergeCand; j++) r += hit_less(cand[j].key_epoch_s, cand[j].idx, h.key_epoch_s, h.idx);
+            if (r == k - 1) {
+                s_wk[0] = h.key_epoch_s;
+                s_wi[0] = h.idx;
+            }
         }
+        __syncthreads();
+        bk = s_wk[0];
+        bi = s_wi[0];
+        if (threadIdx.x == 0) s_nc = 0;
+        __syncthreads();
     }
-    __syncthreads();
     const int nc = s_nc;
     if (nc <= kMergeCand) {
         // rank selection: (key, idx) pairs are distinct, so a candidate's rank is the number
