@@ -70,7 +70,26 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the SURVEY §8(f) next-row sweeps")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = the sweep crossed with N per-GPU FLOP rates (N x the configurations, "
+                         "each rank's shard the size of the 1-GPU sweep); strong = the fixed sweep split N ways")
     return ap.parse_args()
+
+
+def bench_sweep(args, ws: int):
+    """The timed sweep.  N = 1: BASELINE config `args.config` as is.  N > 1 with weak scaling:
+    every sub-sweep crossed with N FLOP rates R0 (1 + r/4), r = 0..N-1 (the paper's system-
+    parameter radix, P:706 'all the permutations of possible configurations'); slice r = 0 is
+    the 1-GPU sweep, and the per-rank top-k are merged over NCCL as in strong scaling."""
+    from workloads import sweeps as W
+    base_sweep = W.CONFIGS[args.config]()
+    if args.scaling == "weak" and ws > 1:
+        R0 = base_sweep.system.flops_per_s
+        for sb in base_sweep.subs:
+            base = list(sb.flops) or [R0]
+            sb.flops = [f * (1.0 + 0.25 * r) for r in range(ws) for f in base]
+        base_sweep.name = f"{base_sweep.name}_x{ws}_flops"
+    return base_sweep
 
 
 # ------------------------------------------------------------------ clocks (nvidia-smi)
@@ -164,7 +183,7 @@ def reference_arm(args):
     if rank != 0:
         return
     from workloads import sweeps as W
-    sweep = W.CONFIGS[args.config]()
+    sweep = bench_sweep(args, dist_env()[0])
     base = {"metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
             "unit": "configs/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
@@ -196,7 +215,7 @@ def reference_arm(args):
                 cpu_baseline={"value": v, "unit": "configs/s", "cores": cores, "kind": "oracle",
                               "sample": f"per step {nwin} windows x 4096 consecutive configs spread over the sweep"},
                 e2e={"value": v, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                vs_baseline=None, scaling="weak")
+                vs_baseline=None, scaling=args.scaling)
     print(json.dumps(line), flush=True)
 
 
@@ -215,7 +234,7 @@ def ours(args):
     import paper_2104_09075_b200 as P
     from workloads import sweeps as W
 
-    sweep = W.CONFIGS[args.config]()
+    sweep = bench_sweep(args, dist_env()[0])
     ctx = P.Context(dev.index)
     spec = ctx.prepare(sweep)
     N = ctx.sweep_size(spec)
@@ -416,7 +435,7 @@ def ours(args):
         line = {
             "metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
             "value": value, "unit": "configs/s", "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": sweep.name, "configs_per_step": N, "k": K_TOP,
                        "model": "+".join(m.name for m in sweep.models) + " layer tables (paper Table 4 shapes)",

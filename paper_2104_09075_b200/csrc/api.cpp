@@ -840,6 +840,10 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const uint64_t nAB = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA];
                 StructJob j{};
                 j.sub = w.sub;
+                j.w_lo = w.lo;
+                j.w_hi = w.hi;
+                j.shard = 0;
+                j.n_shards = 1;   // tile fields set once the tiles are planned
                 j.s_lo = w.lo / nAB;
                 j.n = (w.hi + nAB - 1) / nAB - j.s_lo;
                 w.stab_lo = j.s_lo;
@@ -916,6 +920,14 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             tiles += w.n_tiles;
         }
         a.total_tiles = tiles;
+        for (int i = 0; i < a.n_work; i++)   // structure tables of this launch: shard's tiles only
+            for (StructJob &j : sjobs)
+                if (j.sub == a.work[i].sub && j.w_lo == a.work[i].lo && a.work[i].stab) {
+                    j.ts = 32ull * a.work[i].steps;
+                    j.tile_base = a.work[i].tile_base;
+                    j.shard = shard;
+                    j.n_shards = n_shards;
+                }
         const uint64_t my_tiles = tiles > (uint64_t)shard ? (tiles - shard + n_shards - 1) / n_shards : 0;
         const uint64_t need_ctas = (my_tiles + kWarps - 1) / kWarps;   // small launches: one tile per warp
         grids[li] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid_max, need_ctas));

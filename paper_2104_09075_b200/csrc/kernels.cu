@@ -2957,6 +2957,14 @@ __global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, u
     const uint64_t s_hi = job.s_lo + job.n;
     if (unit * K >= s_hi) return;
     const uint64_t nAB = (uint64_t)S->radix[D_ALPHA] * S->radix[D_BETA];
+    if (job.n_shards > 1) {   // skip units no tile of this shard touches
+        const uint64_t c0 = max(unit * K * nAB, job.w_lo), c1 = min((unit + 1) * K * nAB, job.w_hi);
+        if (c0 >= c1) return;
+        const uint64_t ta = job.tile_base + (c0 - job.w_lo) / job.ts, tb = job.tile_base + (c1 - 1 - job.w_lo) / job.ts;
+        bool need = tb - ta + 1 >= (uint64_t)job.n_shards;
+        for (uint64_t t = ta; !need && t <= tb; t++) need = t % (uint64_t)job.n_shards == (uint64_t)job.shard;
+        if (!need) return;
+    }
     uint16_t cuts[kMaxCuts + 1];
     Lane L;
     decode(v, unit * K * nAB, L, cuts, 1);

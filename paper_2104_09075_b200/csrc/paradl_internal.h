@@ -122,6 +122,10 @@ struct StructJob {
     PipeRec *out;
     unsigned long long *ctr;       // non-null: zero ctr[0, n_ctr) and set ctr[n_ctr] = ~0 (the
     int32_t n_ctr, pad2;           // sweep's tile counters, count and admission bound) first
+    // sharded calls: only structures overlapping this shard's tiles are computed (tile T
+    // covers local configs [w_lo + (T - tile_base) ts, +ts); T % n_shards == shard)
+    uint64_t w_lo, w_hi, ts, tile_base;
+    int32_t shard, n_shards;
 };
 
 // Arguments of one persistent sweep launch (passed as a __grid_constant__ parameter).

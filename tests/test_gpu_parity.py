@@ -236,8 +236,12 @@ def _popcount(x):
     return ((x * 0x01010101) & 0xFFFFFFFF) >> 24
 
 
-def test_sharded_topk_merge_equals_single(dev, oracle_mod):
-    sw = W.config2(n_alpha=8, n_beta=8, b_list=[2, 32, 256], pipe_smax=3)
+@pytest.mark.parametrize("kw", [dict(n_alpha=8, n_beta=8, b_list=[2, 32, 256], pipe_smax=3),
+                                dict(n_alpha=64, n_beta=64, b_list=[8, 64, 256], pipe_smax=3)])
+def test_sharded_topk_merge_equals_single(dev, oracle_mod, kw):
+    """Shards (tile t -> shard t % n) merged on the device equal the single call; the second
+    sweep is large enough for the pipeline structure table, built per shard for its tiles."""
+    sw = W.config2(**kw)
     ctx = P.Context(0)
     spec = ctx.prepare(sw)
     n = ctx.sweep_size(spec)
