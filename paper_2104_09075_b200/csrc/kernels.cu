@@ -1494,6 +1494,8 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                             run_slots<FAM, 2, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                         else if (M2)
                             run_slots<FAM, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
+                        else if (NT == 2)
+                            run_slots<FAM, 1, 2>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                         else
                             run_slots<FAM, 1>(m, tk, alpha_tab, beta_tab, NT, alpha_i, beta_i, run, g0 + lane + 32ull * j);
                     }
