@@ -63,7 +63,7 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one, halo, stab, nvalid;
+    DevBuf img, lists, counters, results, one, halo, stab, nvalid, lists2, nvalid2;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
     std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
@@ -304,6 +304,15 @@ uint64_t binom_u64(int64_t n, int64_t k) {
 }
 
 }  // namespace
+
+// A/B switch for experiments: PARADL_NO_MERGE_LEVEL=1 merges all CTA lists in one block
+static bool merge_level_off() {
+    static const bool off = [] {
+        const char *e = getenv("PARADL_NO_MERGE_LEVEL");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
 
 // A/B switch for experiments: PARADL_NO_STRUCT_TABLE=1 recomputes pipeline structure terms
 // inside the sweep kernel instead of reading the structure table (same results)
@@ -1050,9 +1059,22 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
         cnt = (unsigned long long *)c->counters.p;
         CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     }
-    CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
-                             (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr, 0, 0,
-                             nullptr, nlists ? (const uint32_t *)c->nvalid.p : nullptr));
+    const paradl_hit *mlists = (const paradl_hit *)c->lists.p;
+    const uint32_t *mvalid = nlists ? (const uint32_t *)c->nvalid.p : nullptr;
+    int64_t mn = nlists;
+    if (nlists > 64 && !merge_level_off()) {
+        // many CTA lists: one grouping level first (16 lists per block, no overflow on ties)
+        const int64_t nb = (nlists + 15) / 16;
+        CUDA_TRY(c, c->lists2.ensure(sizeof(paradl_hit) * nb * k));
+        CUDA_TRY(c, c->nvalid2.ensure(sizeof(uint32_t) * nb));
+        CUDA_TRY(c, launch_merge_level(mlists, mvalid, nlists, k, c->last_count_ptr + 1, (paradl_hit *)c->lists2.p,
+                                       (uint32_t *)c->nvalid2.p, st, &mn));
+        c->stat_launches++;
+        mlists = (const paradl_hit *)c->lists2.p;
+        mvalid = (const uint32_t *)c->nvalid2.p;
+    }
+    CUDA_TRY(c, launch_merge(mlists, mn, k, cnt, 1, d_hits, (unsigned long long *)d_n_feasible, st,
+                             nlists ? c->last_count_ptr + 1 : nullptr, 0, 0, nullptr, mvalid));
     c->stat_launches++;
     return PARADL_OK;
 }

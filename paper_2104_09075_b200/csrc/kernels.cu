@@ -3113,6 +3113,56 @@ cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, i
     return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
+// First level of the top-k merge for many CTA lists: block b merges the valid prefixes of
+// lists [16b, 16b + 16) (at most 16 x 64 = 1024 entries: the whole group fits in shared
+// memory, so exact ties cannot overflow anything) by rank selection into one list of at
+// most k entries (its valid length in nvalid_out[b]).  Entries above the shared admission
+// bound's key are dropped first (they can never reach the top k).
+constexpr int kLevelLists = 16;
+__global__ void __launch_bounds__(1024) merge_level_kernel(const paradl_hit *lists, const uint32_t *nvalid,
+                                                            int64_t n_lists, int32_t k,
+                                                            const unsigned long long *gbound, paradl_hit *out,
+                                                            uint32_t *nvalid_out) {
+    __shared__ paradl_hit cand[kLevelLists * PARADL_MAX_TOPK];
+    __shared__ int s_n;
+    const int64_t l0 = (int64_t)blockIdx.x * kLevelLists;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    double gk = CUDART_INF;
+    if (gbound) {
+        const unsigned long long g = *gbound;
+        if (g != ~0ull) gk = __longlong_as_double((long long)g);
+    }
+    {
+        const int li = threadIdx.x / PARADL_MAX_TOPK, j = threadIdx.x % PARADL_MAX_TOPK;
+        const int64_t l = l0 + li;
+        if (li < kLevelLists && l < n_lists && j < (int)nvalid[l]) {
+            const paradl_hit h = lists[l * k + j];
+            if (h.key_epoch_s <= gk) cand[atomicAdd(&s_n, 1)] = h;
+        }
+    }
+    __syncthreads();
+    const int n = s_n;
+    int nv = 0;
+    if (threadIdx.x < n) {
+        const paradl_hit h = cand[threadIdx.x];
+        int r = 0;
+        for (int j = 0; j < n; j++) r += hit_less(cand[j].key_epoch_s, cand[j].idx, h.key_epoch_s, h.idx);
+        if (r < k) out[(int64_t)blockIdx.x * k + r] = h;
+    }
+    nv = min(n, k);
+    if (threadIdx.x == 0) nvalid_out[blockIdx.x] = (uint32_t)nv;
+}
+
+cudaError_t launch_merge_level(const paradl_hit *lists, const uint32_t *nvalid, int64_t n_lists, int32_t k,
+                               const unsigned long long *gbound, paradl_hit *out, uint32_t *nvalid_out,
+                               cudaStream_t st, int64_t *n_out) {
+    const int64_t nb = (n_lists + kLevelLists - 1) / kLevelLists;
+    merge_level_kernel<<<(unsigned)nb, 1024, 0, st>>>(lists, nvalid, n_lists, k, gbound, out, nvalid_out);
+    *n_out = nb;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k, const unsigned long long *counts,
                          int32_t n_counts, paradl_hit *out, unsigned long long *count_out, cudaStream_t st,
                          const unsigned long long *gbound, int32_t lstride, int32_t cstride,
