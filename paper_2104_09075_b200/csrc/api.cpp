@@ -1062,7 +1062,7 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
     const paradl_hit *mlists = (const paradl_hit *)c->lists.p;
     const uint32_t *mvalid = nlists ? (const uint32_t *)c->nvalid.p : nullptr;
     int64_t mn = nlists;
-    if (nlists > 64 && !merge_level_off()) {
+    if (nlists > 512 && !merge_level_off()) {
         // many CTA lists: one grouping level first (16 lists per block, no overflow on ties)
         const int64_t nb = (nlists + 15) / 16;
         CUDA_TRY(c, c->lists2.ensure(sizeof(paradl_hit) * nb * k));
