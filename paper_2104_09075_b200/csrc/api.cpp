@@ -63,7 +63,7 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one, halo, stab, nvalid, lists2, nvalid2;
+    DevBuf img, lists, counters, results, one, halo, stab, nvalid, lists2, nvalid2, mdone;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
     std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
@@ -139,6 +139,11 @@ extern "C" void paradl_destroy(paradl_ctx *c) {
         c->results.release();
         c->one.release();
         c->halo.release();
+        c->stab.release();
+        c->nvalid.release();
+        c->lists2.release();
+        c->nvalid2.release();
+        c->mdone.release();
         for (auto s2 : c->streams) cudaStreamDestroy(s2);
         for (auto e2 : c->events) cudaEventDestroy(e2);
         if (c->fork_ev) cudaEventDestroy(c->fork_ev);
@@ -1059,22 +1064,27 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
         cnt = (unsigned long long *)c->counters.p;
         CUDA_TRY(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     }
-    const paradl_hit *mlists = (const paradl_hit *)c->lists.p;
     const uint32_t *mvalid = nlists ? (const uint32_t *)c->nvalid.p : nullptr;
-    int64_t mn = nlists;
-    if (nlists > 512 && !merge_level_off()) {
-        // many CTA lists: one grouping level first (16 lists per block, no overflow on ties)
+    paradl_hit *lv_out = nullptr;
+    uint32_t *lv_nv = nullptr;
+    unsigned int *lv_done = nullptr;
+    if (nlists > 64 && !merge_level_off()) {
+        // many CTA lists: the merge launch first reduces groups of 16 lists per block (no
+        // overflow on exact ties), its last block merges the group lists
         const int64_t nb = (nlists + 15) / 16;
         CUDA_TRY(c, c->lists2.ensure(sizeof(paradl_hit) * nb * k));
         CUDA_TRY(c, c->nvalid2.ensure(sizeof(uint32_t) * nb));
-        CUDA_TRY(c, launch_merge_level(mlists, mvalid, nlists, k, c->last_count_ptr + 1, (paradl_hit *)c->lists2.p,
-                                       (uint32_t *)c->nvalid2.p, st, &mn));
-        c->stat_launches++;
-        mlists = (const paradl_hit *)c->lists2.p;
-        mvalid = (const uint32_t *)c->nvalid2.p;
+        if (!c->mdone.p) {
+            CUDA_TRY(c, c->mdone.ensure(sizeof(unsigned int)));
+            CUDA_TRY(c, cudaMemsetAsync(c->mdone.p, 0, sizeof(unsigned int), st));
+        }
+        lv_out = (paradl_hit *)c->lists2.p;
+        lv_nv = (uint32_t *)c->nvalid2.p;
+        lv_done = (unsigned int *)c->mdone.p;
     }
-    CUDA_TRY(c, launch_merge(mlists, mn, k, cnt, 1, d_hits, (unsigned long long *)d_n_feasible, st,
-                             nlists ? c->last_count_ptr + 1 : nullptr, 0, 0, nullptr, mvalid));
+    CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
+                             (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr, 0, 0,
+                             nullptr, mvalid, lv_out, lv_nv, lv_done));
     c->stat_launches++;
     return PARADL_OK;
 }

@@ -2494,6 +2494,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
 // thread per list collects them (early exit, lists are sorted), then one warp selects.
 constexpr int kMergeCand = 1536;
 constexpr int kMergeLists = 4096;   // lists whose valid-prefix offsets fit the shared scan
+constexpr int kLevelLists = 16;     // lists per block of the first merge level
 
 __device__ __forceinline__ void hit_min(double &k, uint64_t &i, double k2, uint64_t i2) {
     if (hit_less(k2, i2, k, i)) {
@@ -2507,7 +2508,8 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
                                                       paradl_hit *out, unsigned long long *count_out,
                                                       const unsigned long long *gbound, int32_t lstride,
                                                       int32_t cstride, unsigned long long *bound_out,
-                                                      const uint32_t *nvalid) {
+                                                      const uint32_t *nvalid, paradl_hit *lv_out,
+                                                      uint32_t *lv_nvalid, unsigned int *lv_done) {
     __shared__ paradl_hit cand[kMergeCand];
     __shared__ uint32_t s_pre[kMergeLists + 1];
     __shared__ unsigned long long s_cnt;
@@ -2515,6 +2517,47 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     __shared__ uint64_t s_wi[32];
     __shared__ int s_nc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lv_out) {
+        // fused first level (gridDim.x blocks, 16 lists each, rank selection of at most 1024
+        // entries in shared memory: exact ties cannot overflow), then the last block to
+        // finish merges the gridDim.x level lists below (threadfence + ticket)
+        if (threadIdx.x == 0) s_nc = 0;
+        __syncthreads();
+        double gk = CUDART_INF;
+        if (gbound) {
+            const unsigned long long g = *gbound;
+            if (g != ~0ull) gk = __longlong_as_double((long long)g);
+        }
+        {
+            const int li = threadIdx.x / PARADL_MAX_TOPK, j = threadIdx.x % PARADL_MAX_TOPK;
+            const int64_t l = (int64_t)blockIdx.x * kLevelLists + li;
+            if (li < kLevelLists && l < n_lists && j < (int)nvalid[l]) {
+                const paradl_hit h = lists[l * lstride + j];
+                if (h.key_epoch_s <= gk) cand[atomicAdd(&s_nc, 1)] = h;
+            }
+        }
+        __syncthreads();
+        const int n = s_nc;
+        if (threadIdx.x < n) {
+            const paradl_hit h = cand[threadIdx.x];
+            int r = 0;
+            for (int j = 0; j < n; j++) r += hit_less(cand[j].key_epoch_s, cand[j].idx, h.key_epoch_s, h.idx);
+            if (r < k) lv_out[(int64_t)blockIdx.x * k + r] = h;
+        }
+        if (threadIdx.x == 0) lv_nvalid[blockIdx.x] = (uint32_t)min(n, k);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_nc = atomicAdd(lv_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!s_nc) return;
+        __threadfence();
+        if (threadIdx.x == 0) *lv_done = 0u;   // ready for the next call
+        lists = lv_out;
+        nvalid = lv_nvalid;
+        n_lists = gridDim.x;
+        lstride = k;
+        __syncthreads();
+    }
     const unsigned full = 0xffffffffu;
     if (threadIdx.x == 0) {
         s_cnt = 0;
@@ -3113,62 +3156,15 @@ cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, i
     return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
-// First level of the top-k merge for many CTA lists: block b merges the valid prefixes of
-// lists [16b, 16b + 16) (at most 16 x 64 = 1024 entries: the whole group fits in shared
-// memory, so exact ties cannot overflow anything) by rank selection into one list of at
-// most k entries (its valid length in nvalid_out[b]).  Entries above the shared admission
-// bound's key are dropped first (they can never reach the top k).
-constexpr int kLevelLists = 16;
-__global__ void __launch_bounds__(1024) merge_level_kernel(const paradl_hit *lists, const uint32_t *nvalid,
-                                                            int64_t n_lists, int32_t k,
-                                                            const unsigned long long *gbound, paradl_hit *out,
-                                                            uint32_t *nvalid_out) {
-    __shared__ paradl_hit cand[kLevelLists * PARADL_MAX_TOPK];
-    __shared__ int s_n;
-    const int64_t l0 = (int64_t)blockIdx.x * kLevelLists;
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-    double gk = CUDART_INF;
-    if (gbound) {
-        const unsigned long long g = *gbound;
-        if (g != ~0ull) gk = __longlong_as_double((long long)g);
-    }
-    {
-        const int li = threadIdx.x / PARADL_MAX_TOPK, j = threadIdx.x % PARADL_MAX_TOPK;
-        const int64_t l = l0 + li;
-        if (li < kLevelLists && l < n_lists && j < (int)nvalid[l]) {
-            const paradl_hit h = lists[l * k + j];
-            if (h.key_epoch_s <= gk) cand[atomicAdd(&s_n, 1)] = h;
-        }
-    }
-    __syncthreads();
-    const int n = s_n;
-    int nv = 0;
-    if (threadIdx.x < n) {
-        const paradl_hit h = cand[threadIdx.x];
-        int r = 0;
-        for (int j = 0; j < n; j++) r += hit_less(cand[j].key_epoch_s, cand[j].idx, h.key_epoch_s, h.idx);
-        if (r < k) out[(int64_t)blockIdx.x * k + r] = h;
-    }
-    nv = min(n, k);
-    if (threadIdx.x == 0) nvalid_out[blockIdx.x] = (uint32_t)nv;
-}
-
-cudaError_t launch_merge_level(const paradl_hit *lists, const uint32_t *nvalid, int64_t n_lists, int32_t k,
-                               const unsigned long long *gbound, paradl_hit *out, uint32_t *nvalid_out,
-                               cudaStream_t st, int64_t *n_out) {
-    const int64_t nb = (n_lists + kLevelLists - 1) / kLevelLists;
-    merge_level_kernel<<<(unsigned)nb, 1024, 0, st>>>(lists, nvalid, n_lists, k, gbound, out, nvalid_out);
-    *n_out = nb;
-    return cudaGetLastError();
-}
-
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k, const unsigned long long *counts,
                          int32_t n_counts, paradl_hit *out, unsigned long long *count_out, cudaStream_t st,
                          const unsigned long long *gbound, int32_t lstride, int32_t cstride,
-                         unsigned long long *bound_out, const uint32_t *nvalid) {
-    merge_kernel<<<1, 1024, 0, st>>>(lists, n_lists, k, counts, n_counts, out, count_out, gbound,
-                                     lstride > 0 ? lstride : k, cstride > 0 ? cstride : 1, bound_out, nvalid);
+                         unsigned long long *bound_out, const uint32_t *nvalid, paradl_hit *lv_out,
+                         uint32_t *lv_nvalid, unsigned int *lv_done) {
+    const unsigned grid = lv_out ? (unsigned)((n_lists + kLevelLists - 1) / kLevelLists) : 1u;
+    merge_kernel<<<grid, 1024, 0, st>>>(lists, n_lists, k, counts, n_counts, out, count_out, gbound,
+                                        lstride > 0 ? lstride : k, cstride > 0 ? cstride : 1, bound_out, nvalid,
+                                        lv_out, lv_nvalid, lv_done);
     return cudaGetLastError();
 }
 

@@ -174,11 +174,9 @@ cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,
                          unsigned long long *count_out, cudaStream_t st,
                          const unsigned long long *gbound = nullptr, int32_t lstride = 0, int32_t cstride = 0,
-                         unsigned long long *bound_out = nullptr, const uint32_t *nvalid = nullptr);
+                         unsigned long long *bound_out = nullptr, const uint32_t *nvalid = nullptr,
+                         paradl_hit *lv_out = nullptr, uint32_t *lv_nvalid = nullptr, unsigned int *lv_done = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
-cudaError_t launch_merge_level(const paradl_hit *lists, const uint32_t *nvalid, int64_t n_lists, int32_t k,
-                               const unsigned long long *gbound, paradl_hit *out, uint32_t *nvalid_out,
-                               cudaStream_t st, int64_t *n_out);
 cudaError_t launch_struct_table(const uint8_t *img, uint32_t img_bytes, const StructJob &job, uint64_t unit_len,
                                 cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);
