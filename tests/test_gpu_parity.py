@@ -36,7 +36,8 @@ def rel_err(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     both_inf = np.isinf(a) & np.isinf(b) & (np.sign(a) == np.sign(b))
-    d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
+    with np.errstate(invalid="ignore"):   # inf - inf: same-sign infinities are zeroed below
+        d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
     d[both_inf] = 0.0
     d[(a == b)] = 0.0
     return d
