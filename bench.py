@@ -1,17 +1,21 @@
 #!/usr/bin/env python3
 """bench.py -- configurations evaluated per second by the ParaDL sweep on 1..8 B200.
 
-Workload (BASELINE.json configs[1]): ResNet-50, six strategies
-(data, spatial, filter, channel, data+filter, data+spatial, pipeline s<=4) x b in 2^0..2^8
-x a 64x64 alpha/beta grid = 2,914,136,064 configurations per step.  A step is one pass of
-the hot path over the whole sweep: decode -> Table 2 cost -> feasibility -> top-64 /
-argmin / feasible count, per rank over its tile shard, then (N > 1) one NCCL all_gather
-of the per-rank top-k and the device merge.  `value` = configurations / s for the whole
-job (inputs resident: model + spec image loaded before the timed region); `e2e` = the
-same through the public C-ABI with host inputs and host results (paradl_set_system +
+Headline workload (BASELINE.json configs[4], the largest sweep that is
+also the 8-GPU target): ResNet-152 pipeline + data parallelism -- every contiguous partition of
+the 152 rows into s <= 6 stages (633,245,832 partitions) x S in {1,2,4,8} x p_d in 2^0..2^7 x
+a 2 x 2 alpha/beta grid = 81,055,466,496 configurations per step.  A step is one pass of the
+hot path over the whole sweep: decode -> Table 2 cost -> feasibility -> top-64 / argmin /
+feasible count, per rank over its tile shard, then (N > 1) one NCCL all_gather of the
+per-rank top-k records and the device merge.  N > 1 defaults to strong scaling (the fixed
+sweep split N ways); `--scaling weak` crosses the sweep with N FLOP rates instead and is
+reported under a different metric name.  `value` = configurations / s for the whole job
+(inputs resident: model + spec image loaded before the timed region); `e2e` = the same
+through the public C-ABI with host inputs and host results (paradl_set_system +
 paradl_topk each step, which re-uploads the spec image and reads back the hits).
+`configs` = the other BASELINE configs (1-4) timed the same way, one line each.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5]
 Under torchrun (N > 1) each rank drives LOCAL_RANK's GPU; rank 0 prints one JSON line.
 """
 from __future__ import annotations
@@ -30,6 +34,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 K_TOP = 64
+METRIC = "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline"
+METRIC_WEAK = METRIC + " [weak scaling: the sweep crossed with N FLOP rates, N x the configurations]"
 # Algorithmic FP64-pipe instructions per configuration: the alpha/beta-dependent increment of
 # the canonical tree after hoisting what is invariant over the inner radices
 # (s*beta is formed once per beta slot, alpha-side products once per alpha row and shared by
@@ -52,6 +58,11 @@ def fp64_per_config(sb) -> float:
     from workloads import sweeps as W
     fam = W.FAMILY_NAMES[sb.family]
     nab = max(1, len(sb.alpha)) * max(1, len(sb.beta))
+    if fam == "pipeline" and sb.part_mode == W.PART_MASK and nab * max(1, len(sb.S)) * max(1, len(sb.dims)) == 1:
+        # one configuration per mask (cfg3-ii): every configuration is its own structure, so the
+        # whole canonical tree runs per configuration except its per-stage-count constants
+        # (cseg, pp_c): (cseg FB) tau, U tau, +, bS D(delta maxY), * beta, alpha +, pp_c *, comp + P, * I
+        return 10.0
     if fam in ("pd", "pipeline") and nab < 32:
         n_s, n_d = max(1, len(sb.S)), max(1, len(sb.dims))
         g = 3.0 * math.ceil(n_s / 4) / n_s if fam == "pd" else 0.0
@@ -62,17 +73,19 @@ def fp64_per_config(sb) -> float:
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the SURVEY §8(f) next-row sweeps")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = the sweep crossed with N per-GPU FLOP rates (N x the configurations, "
-                         "each rank's shard the size of the 1-GPU sweep); strong = the fixed sweep split N ways")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the fixed sweep split N ways (default, the headline metric); weak = "
+                         "the sweep crossed with N per-GPU FLOP rates (N x the configurations, each rank's shard "
+                         "the size of the 1-GPU sweep), reported under a separate metric name")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines for the other BASELINE configs")
     return ap.parse_args()
 
 
@@ -151,6 +164,40 @@ def dist_env():
     return ws, rank, local
 
 
+def cpu_model() -> str:
+    """Host CPU model name (lscpu 'Model name', else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def golden_check(cfg: int, sweep, n: int, hits, n_feasible: int):
+    """Compares a whole-sweep top-k with the oracle golden tests/golden/full_cfgN.json (written
+    offline by tools/golden_full.py from oracle/ alone; a stored file, the oracle is not run).
+    None when no golden exists for this workload."""
+    path = os.path.join(ROOT, "tests", "golden", f"full_cfg{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    g = json.load(open(path))
+    if g.get("workload") != sweep.name or g.get("configs") != n:
+        return None
+    gh = [(i, float.fromhex(k)) for i, k in g["hits"]]
+    ours = [(int(i), float(k)) for i, k in hits[:len(gh)]]
+    return {"golden": os.path.relpath(path, ROOT), "topk_identical": ours == gh,
+            "count_identical": int(n_feasible) == int(g["n_feasible"]), "k": len(gh)}
+
+
 def cpu_oracle_baseline(sweep, target_s: float, rank: int = 0):
     """The oracle as it stands, on all host cores, on a bounded sample of the same sweep:
     contiguous windows of 4096 configurations at evenly spaced offsets."""
@@ -173,7 +220,7 @@ def cpu_oracle_baseline(sweep, target_s: float, rank: int = 0):
     tot, dt = run(8)
     nwin = max(8, int(8 * target_s / max(dt, 1e-3)))
     tot, dt = run(nwin)
-    return {"value": tot / dt, "unit": "configs/s", "cores": cores, "kind": "oracle",
+    return {"value": tot / dt, "unit": "configs/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{nwin} windows x 4096 consecutive configs evenly spaced over the {n}-config sweep "
                       f"({tot} configs, {dt:.1f} s, top-{K_TOP} + count per window)"}
 
@@ -184,7 +231,7 @@ def reference_arm(args):
         return
     from workloads import sweeps as W
     sweep = bench_sweep(args, dist_env()[0])
-    base = {"metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
+    base = {"metric": METRIC if args.scaling == "strong" or args.gpus <= 1 else METRIC_WEAK,
             "unit": "configs/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
             "config": {"workload": sweep.name}}
@@ -212,7 +259,7 @@ def reference_arm(args):
             tot += nwin * 4096
     v = tot / sum(times)
     line = dict(base, value=v, ms_per_step=1e3 * sum(times) / len(times),
-                cpu_baseline={"value": v, "unit": "configs/s", "cores": cores, "kind": "oracle",
+                cpu_baseline={"value": v, "unit": "configs/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                               "sample": f"per step {nwin} windows x 4096 consecutive configs spread over the sweep"},
                 e2e={"value": v, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 vs_baseline=None, scaling=args.scaling)
@@ -293,6 +340,8 @@ def ours(args):
     gpu_launches = launches[0]
     best = res.cpu().numpy()
     n_feasible = int(rc.item())
+    best_hits = [(int(i) % (1 << 64), float(k)) for i, k in zip(best[:, 0], best[:, 1].view("float64"))]
+    gold = golden_check(args.config, sweep, N, best_hits, n_feasible) if args.scaling == "strong" or ws == 1 else None
 
     # ---- e2e: public C-ABI, host inputs (spec image re-uploaded) and host results
     e2e_ms = []
@@ -369,7 +418,15 @@ def ours(args):
                 traffic = json.load(open(tp)).get(f"sweep_kernel_{fam_name}_bytes_per_launch")
             except Exception:
                 traffic = None
+        ncu_fp = None
+        fp_path = os.path.join(ROOT, "profiles", "fp64_ncu.json")
+        if os.path.exists(fp_path):
+            try:
+                ncu_fp = json.load(open(fp_path)).get(sweep.name, {}).get(fam_name)
+            except Exception:
+                ncu_fp = None
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T fp64-pipe inst/s",
+                "fp64_inst_per_config_ncu": ncu_fp,
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": f"sweep_kernel<{fam_name.upper()},reduce> (+merge)", "configs_per_launch": nd,
                 "fp64_inst_per_config": opc, "feasible_configs": n_feas,
@@ -427,13 +484,18 @@ def ours(args):
         nxt = next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak)
         ctx.set_system(sweep.system)
 
+    per_cfg = None
+    if ws == 1 and not args.no_configs:
+        per_cfg = config_lines(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak, args.config)
+        ctx.set_system(sweep.system)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(sweep, args.cpu_seconds)
 
     if rank == 0:
         line = {
-            "metric": "oracle configs evaluated/sec at 1/2/4/8 B200; % of FP64 issue roofline",
+            "metric": METRIC if args.scaling == "strong" or ws == 1 else METRIC_WEAK,
             "value": value, "unit": "configs/s", "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -447,13 +509,76 @@ def ours(args):
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "dense": dense,
             "next_rows": nxt,
-            "result": {"argmin_idx": int(best[0, 0]) % (1 << 64), "n_feasible": n_feasible},
+            "result": {"argmin_idx": int(best[0, 0]) % (1 << 64), "n_feasible": n_feasible, "vs_oracle_golden": gold},
+            "configs": per_cfg,
             "fp64_peak_inst_per_s": fp64_peak,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def dominant_roofline(ctx, P, W, sweep, spec, stream, flush, my_hits, my_cnt, fp64_peak, reps=3):
+    """FP64 roofline of the largest sub-sweep of `sweep`, timed alone (L2 flushed)."""
+    import torch
+    sizes = [(ctx.sweep_size(sub_spec(P, spec, sweep, i)), i) for i in range(len(sweep.subs))]
+    nd, di = max(sizes)
+    dspec = sub_spec(P, spec, sweep, di)
+    fam = W.FAMILY_NAMES[sweep.subs[di].family]
+    ctx.topk_async(dspec, 0, nd, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+    ev = []
+    for _ in range(reps):
+        flush.fill_(5)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        ctx.topk_async(dspec, 0, nd, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        b_.record(stream)
+        ev.append((a_, b_))
+    torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    nf = int(my_cnt.item())
+    opc = fp64_per_config(sweep.subs[di])
+    ach = nf * opc / (ms * 1e-3) / 1e12
+    return {"bound": "alu", "kernel": f"sweep_kernel<{fam.upper()},reduce>", "sub_sweep_configs": nd,
+            "launch_ms": ms, "fp64_inst_per_config": opc, "achieved": ach, "peak": fp64_peak / 1e12,
+            "unit": "T fp64-pipe inst/s", "frac": ach / (fp64_peak / 1e12)}
+
+
+def config_lines(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak, headline):
+    """The other BASELINE configs, each one whole-sweep top-64 + count per
+    step timed like the headline (L2 flushed before each timed launch), with the FP64 roofline
+    of its largest sub-sweep and the comparison with its oracle golden where one exists."""
+    import torch
+    out = {}
+    for cfg in sorted(W.CONFIGS):
+        if cfg == headline:
+            continue
+        sw = W.CONFIGS[cfg]()
+        spec = ctx.prepare(sw)
+        n = ctx.sweep_size(spec)
+        reps = 3 if n > 5e10 else 10
+        ctx.topk_async(spec, 0, n, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+        evs = []
+        for _ in range(reps):
+            flush.fill_(4)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            ctx.topk_async(spec, 0, n, 0, 1, K_TOP, my_hits.data_ptr(), my_cnt.data_ptr(), stream=stream)
+            b_.record(stream)
+            evs.append((a_, b_))
+        torch.cuda.synchronize()
+        ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+        nf = int(my_cnt.item())
+        h = my_hits.cpu().numpy()
+        hits = [(int(i) % (1 << 64), float(k)) for i, k in zip(h[:, 0], h[:, 1].view("float64"))]
+        line = {"workload": sw.name, "configs": n, "ms": ms, "configs_per_s": n / (ms * 1e-3),
+                "result": {"argmin_idx": hits[0][0], "n_feasible": nf,
+                           "vs_oracle_golden": golden_check(cfg, sw, n, hits, nf)}}
+        if n > 1000:
+            line["roofline"] = dominant_roofline(ctx, P, W, sw, spec, stream, flush, my_hits, my_cnt, fp64_peak)
+        out[f"cfg{cfg}"] = line
+    return out
 
 
 def gpipe_ops(s: int, S: int) -> int:

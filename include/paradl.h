@@ -193,12 +193,36 @@ typedef struct {
     int32_t feasible;
 } paradl_prediction;
 
+/* Compact outputs for the feasible configurations of [first, first+count), in ascending
+ * index order (row a9 compact mode; the per-configuration breakdown of P:427-429 restricted
+ * to what fits the PEs).  All DEVICE pointers, caller-allocated:
+ *   idx: capacity uint64, global configuration indices, strictly ascending
+ *   t_iter, mem: capacity doubles each (may be NULL: not written), as in paradl_dense_out
+ *   n_feasible: one uint64, the number of feasible configurations in the range; entries past
+ *     `capacity` are not written (the caller compares *n_feasible with capacity). */
+typedef struct {
+    uint64_t *idx;
+    double *t_iter;
+    double *mem;
+    uint64_t capacity;
+    uint64_t *n_feasible;
+} paradl_compact_out;
+
 /* Number of configurations of the sweep (host-only ctx allowed). */
 paradl_status paradl_sweep_size(paradl_ctx *ctx, const paradl_sweep_spec *spec, uint64_t *n);
 
 /* Dense evaluation, asynchronous on `stream`. */
 paradl_status paradl_sweep(paradl_ctx *ctx, const paradl_sweep_spec *spec, uint64_t first,
                            uint64_t count, const paradl_dense_out *out, void *stream);
+
+/* Compact evaluation, asynchronous on `stream`: two passes over the same tiles -- the first
+ * counts the feasible configurations of every tile (warp ballots), an exclusive scan over the
+ * tiles in index order gives each tile its output offset, the second re-evaluates the tiles
+ * and writes (idx, t_iter, mem) at offset + popc(ballot & lanes below) (coalesced SoA stores).
+ * The values equal paradl_sweep's for the same configurations.  Errors: as paradl_sweep;
+ * PARADL_EINVAL for a NULL idx or n_feasible. */
+paradl_status paradl_sweep_compact(paradl_ctx *ctx, const paradl_sweep_spec *spec, uint64_t first,
+                                   uint64_t count, const paradl_compact_out *out, void *stream);
 
 /* Top-k (1 <= k <= PARADL_MAX_TOPK) of the feasible configurations of [first, first+count)
  * by (key, idx), plus their count.  Host outputs; synchronises `stream`. */

@@ -188,6 +188,12 @@ class Context:
         out = A.DenseOut(t_iter_ptr or None, mem_ptr or None, bits_ptr or None, reason_ptr or None)
         self._check(_lib.paradl_sweep(self._h, spec.ref, first, count, C.byref(out), _stream(stream)))
 
+    def sweep_compact(self, spec: Spec, first: int, count: int, idx_ptr: int, capacity: int, n_ptr: int,
+                      t_iter_ptr=0, mem_ptr=0, stream=None):
+        """Feasible configurations of [first, first+count) in index order (device outputs)."""
+        out = A.CompactOut(idx_ptr, t_iter_ptr or None, mem_ptr or None, capacity, n_ptr)
+        self._check(_lib.paradl_sweep_compact(self._h, spec.ref, first, count, C.byref(out), _stream(stream)))
+
     def stat(self, which: int) -> int:
         """0: H2D bytes, 1: D2H bytes, 2: kernel launches of the last call."""
         return int(_lib.paradl_stat(self._h, which))

@@ -54,6 +54,11 @@ class DenseOut(C.Structure):
                 ("reason", C.c_void_p)]
 
 
+class CompactOut(C.Structure):
+    _fields_ = [("idx", C.c_void_p), ("t_iter", C.c_void_p), ("mem", C.c_void_p), ("capacity", C.c_uint64),
+                ("n_feasible", C.c_void_p)]
+
+
 class Hit(C.Structure):
     _fields_ = [("idx", C.c_uint64), ("key_epoch_s", C.c_double)]
 
@@ -86,7 +91,7 @@ STRUCTS = [Layer, System, SubSweep, Config, Prediction, Hit]
 EXPORTS = ["paradl_create", "paradl_destroy", "paradl_last_error", "paradl_version", "paradl_load_model",
            "paradl_set_system", "paradl_sweep_size", "paradl_sweep", "paradl_topk", "paradl_argmin",
            "paradl_topk_async", "paradl_merge_topk", "paradl_decode", "paradl_explain", "paradl_struct_size",
-           "paradl_stat", "paradl_fp64_peak", "paradl_merge_records"]
+           "paradl_stat", "paradl_fp64_peak", "paradl_merge_records", "paradl_sweep_compact"]
 
 
 def declare(lib):
@@ -102,6 +107,7 @@ def declare(lib):
     lib.paradl_set_system.argtypes = [vp, P(System)]
     lib.paradl_sweep_size.argtypes = [vp, P(SweepSpec), P(C.c_uint64)]
     lib.paradl_sweep.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, P(DenseOut), vp]
+    lib.paradl_sweep_compact.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, P(CompactOut), vp]
     lib.paradl_topk.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, C.c_int32, P(Hit), P(C.c_uint64), vp]
     lib.paradl_argmin.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, P(Hit), P(C.c_uint64), vp]
     lib.paradl_topk_async.argtypes = [vp, P(SweepSpec), C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32,

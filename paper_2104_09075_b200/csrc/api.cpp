@@ -52,6 +52,12 @@ struct DevBuf {
 
 constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// One pass of paradl_sweep_compact through run_sweep (see there)
+struct CompactCall {
+    int pass;                        // 1: count per tile + scan; 2: write
+    const paradl_compact_out *out;
+};
+
 }  // namespace
 
 struct paradl_ctx {
@@ -63,7 +69,7 @@ struct paradl_ctx {
     paradl_system sys{};
     std::vector<HostModel> models;
     // device scratch
-    DevBuf img, lists, counters, results, one, halo, stab, nvalid, lists2, nvalid2, mdone;
+    DevBuf img, lists, counters, results, one, halo, stab, nvalid, lists2, nvalid2, ccnt, coff;
     std::vector<uint8_t> last_img;     // host copy of the image currently on the device
     uint64_t stat_h2d = 0, stat_d2h = 0, stat_launches = 0;
     std::vector<cudaStream_t> streams;     // internal fork streams (one per family launch)
@@ -140,10 +146,11 @@ extern "C" void paradl_destroy(paradl_ctx *c) {
         c->one.release();
         c->halo.release();
         c->stab.release();
+        c->ccnt.release();
+        c->coff.release();
         c->nvalid.release();
         c->lists2.release();
         c->nvalid2.release();
-        c->mdone.release();
         for (auto s2 : c->streams) cudaStreamDestroy(s2);
         for (auto e2 : c->events) cudaEventDestroy(e2);
         if (c->fork_ev) cudaEventDestroy(c->fork_ev);
@@ -319,6 +326,12 @@ static bool merge_level_off() {
     return off;
 }
 
+// A/B switch for experiments: PARADL_NO_COMB=1 keeps COMB pipeline / pd sweeps on mode 1
+// (tile_body_blocked) instead of mode 3 (tile_body_comb); same results
+static bool comb_off() {
+    static const bool off = getenv("PARADL_NO_COMB") != nullptr;
+    return off;
+}
 // A/B switch for experiments: PARADL_NO_STRUCT_TABLE=1 recomputes pipeline structure terms
 // inside the sweep kernel instead of reading the structure table (same results)
 static bool struct_table_off() {
@@ -667,7 +680,8 @@ static void stride_digits(const SubHdr &h, WorkItem &a) {
 // caller's stream then waits for all of them.  Per-CTA top-k lists land contiguously in
 // c->lists (reduce mode); *n_lists_out = total CTAs.
 static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uint64_t count, int shard, int n_shards,
-                               bool dense, int k, const paradl_dense_out *out, cudaStream_t st, int *n_lists_out) {
+                               bool dense, int k, const paradl_dense_out *out, cudaStream_t st, int *n_lists_out,
+                               const CompactCall *cmp = nullptr) {
     const size_t smem = P.bytes + sweep_smem_extra();
     std::vector<LaunchArgs> L;
     std::vector<int> fam_of;
@@ -704,9 +718,18 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         const uint64_t maskd_n = (mask2 && fam == PARADL_PIPELINE && Q == 1) ? h.radix[D_B] * 4ull * kMaskTabN : 0;
         const uint64_t memo_n =
             (uint64_t)h.radix[D_B] * (h.radix[D_S] + h.radix[D_DIMS]) + ctab_n + (ctab_n + 1) / 2 + maskd_n;
-        const int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22))
-                             ? (mask2 ? 2 : 1)
-                             : 0;
+        int mode = (!dense && pipe && nAB < 32 && memo_n <= 2048 && Q < (1ull << 22))
+                       ? (mask2 ? 2 : 1)
+                       : 0;
+        // mode 3 (tile_body_comb): COMB pipeline / pd with ring collectives and <= 2 x 2
+        // alpha/beta rows -- incremental stage terms, per-(b, s, S) / (b, s, dims) tables
+        const uint64_t ns1 = (uint64_t)h.s_max + 1;
+        const uint64_t cmb_bytes = ns1 * 48 + (uint64_t)h.radix[D_B] * ns1 * (h.radix[D_S] * 32ull + h.radix[D_DIMS] * 64ull);
+        if (mode == 1 && h.part_mode == PARADL_PART_COMB && (fam == PARADL_PIPELINE || fam == PARADL_PD) &&
+            (fam == PARADL_PIPELINE || c->sys.tree_threshold_B <= 0.0) && h.radix[D_ALPHA] <= 2 &&
+            h.radix[D_BETA] <= 2 && cmb_bytes <= (32u << 10) && !comb_off() &&
+            smem + kLaneStateBytes + cmb_bytes + memo_n * sizeof(double) + 1024 <= c->smem_optin)
+            mode = 3;
         const uint64_t unit = mode == 2 ? Q << 8 : Q;
         const uint64_t lo = r0 - s0, hi = r1 - s0;
         uint64_t b0 = lo, b1 = lo;   // [b0, b1): blocked part
@@ -740,6 +763,10 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 w.memo_n = (uint32_t)memo_n;
                 w.memo_off = a.memo_bytes;
                 a.memo_bytes += (uint32_t)align16(memo_n * sizeof(double));
+                if (mode == 3) {
+                    w.cmb_off = a.memo_bytes;
+                    a.memo_bytes += (uint32_t)align16(cmb_bytes);
+                }
                 if (mode == 1 && (fam == PARADL_PIPELINE || fam == PARADL_PD)) {
                     // screened path: per-lane dims table (ge_c, ge_s fp64 + ge_t u8) per thread
                     const uint32_t nD = h.radix[D_DIMS];
@@ -797,7 +824,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     {
         const size_t n0 = L.size();
         for (size_t li = 0; li < n0; li++) {
-            LaunchArgs by_mode[3];
+            LaunchArgs by_mode[4];
             for (auto &x : by_mode) memset(&x, 0, sizeof x);
             for (int i = 0; i < L[li].n_work; i++) {
                 const WorkItem &w = L[li].work[i];
@@ -805,13 +832,13 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             }
             bool first = true;
             const uint32_t memo_bytes = L[li].memo_bytes, low_bytes = L[li].low_bytes, dtab_bytes = L[li].dtab_bytes;
-            for (int md = 0; md < 3; md++) {
+            for (int md = 0; md < 4; md++) {
                 LaunchArgs &x = by_mode[md];
                 if (x.n_work == 0) continue;
                 if (md) {
                     x.memo_bytes = memo_bytes;
                     x.low_bytes = low_bytes;
-                    x.dtab_bytes = md == 1 ? dtab_bytes : 0;
+                    x.dtab_bytes = md == 1 ? dtab_bytes : md == 3 ? kLaneStateBytes : 0;
                 } else if (fam_of[li] == PARADL_GPIPE) {
                     x.dtab_bytes = dtab_bytes;   // per-lane stage table
                 } else if (fam_of[li] == PARADL_DATA_LW) {
@@ -886,8 +913,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
         if (smem + a.memo_bytes + a.low_bytes + a.dtab_bytes > c->smem_optin) {
-            if (fam_of[li] == PARADL_GPIPE)
-                return fail(c, PARADL_ENOMEM, "image + gpipe stage table exceed shared memory");
+            if (fam_of[li] == PARADL_GPIPE || blk_of[li] == 3)
+                return fail(c, PARADL_ENOMEM, "image + per-lane tables exceed shared memory");
             a.dtab_bytes = 0;   // unscreened path
         }
         smems[li] = smem + a.memo_bytes + a.low_bytes + a.dtab_bytes;
@@ -947,7 +974,34 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         grids[li] = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid_max, need_ctas));
         total_ctas += grids[li];
     }
-    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 2)));
+    // counters: [nl] tile queues, [nl] count, [nl + 1] admission bound, [nl + 2] merge ticket
+    // compact mode: the launches' tile spaces concatenated (slot_base[li] + T), and the tile
+    // segments of every work item in ascending index order for the scan
+    std::vector<uint64_t> slot_base(nl, 0);
+    uint64_t n_slots = 0;
+    CompactSegs segs{};
+    if (cmp) {
+        for (size_t li = 0; li < nl; li++) {
+            slot_base[li] = n_slots;
+            n_slots += L[li].total_tiles;
+        }
+        std::vector<std::pair<uint64_t, std::pair<uint64_t, uint64_t>>> order;
+        for (size_t li = 0; li < nl; li++)
+            for (int i = 0; i < L[li].n_work; i++) {
+                const WorkItem &w = L[li].work[i];
+                order.push_back({P.subs[w.sub].hdr.offset + w.lo, {slot_base[li] + w.tile_base, w.n_tiles}});
+            }
+        std::sort(order.begin(), order.end());
+        if (order.size() > (size_t)kMaxSegs) return fail(c, PARADL_EINVAL, "compact sweep: too many work items");
+        segs.n = (int32_t)order.size();
+        for (size_t g = 0; g < order.size(); g++) {
+            segs.slot[g] = order[g].second.first;
+            segs.cnt[g] = order[g].second.second;
+        }
+        CUDA_TRY(c, c->ccnt.ensure(sizeof(uint32_t) * std::max<uint64_t>(1, n_slots)));
+        CUDA_TRY(c, c->coff.ensure(sizeof(uint64_t) * std::max<uint64_t>(1, n_slots)));
+    }
+    CUDA_TRY(c, c->counters.ensure(sizeof(unsigned long long) * (nl + 3)));
     if (!dense) CUDA_TRY(c, c->lists.ensure(sizeof(paradl_hit) * total_ctas * k));
     if (!dense) CUDA_TRY(c, c->nvalid.ensure(sizeof(uint32_t) * total_ctas));
     unsigned long long *ctr = (unsigned long long *)c->counters.p;
@@ -955,7 +1009,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         sjobs[0].ctr = ctr;
         sjobs[0].n_ctr = (int32_t)(nl + 1);
     } else {
-        CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 1), st));
+        CUDA_TRY(c, cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * (nl + 3), st));
         CUDA_TRY(c, cudaMemsetAsync(ctr + nl + 1, 0xFF, sizeof(unsigned long long), st));   // no bound yet
     }
 
@@ -997,7 +1051,17 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         a.k = k;
         a.cta_lists = dense ? nullptr : (paradl_hit *)c->lists.p + cta_off * k;
         a.cta_nvalid = dense ? nullptr : (uint32_t *)c->nvalid.p + cta_off;
-        if (dense) {
+        if (dense && cmp) {
+            if (cmp->pass == 1) {
+                a.c_cnt = (uint32_t *)c->ccnt.p + slot_base[li];
+            } else {
+                a.c_off = (const uint64_t *)c->coff.p + slot_base[li];
+                a.c_idx = cmp->out->idx;
+                a.c_cap = cmp->out->capacity;
+                a.t_iter = cmp->out->t_iter;
+                a.mem = cmp->out->mem;
+            }
+        } else if (dense) {
             a.t_iter = out->t_iter;
             a.mem = out->mem;
             a.bits = out->feasible_bits;
@@ -1015,6 +1079,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     }
     if (fork)
         for (size_t li = 0; li < nl; li++) CUDA_TRY(c, cudaStreamWaitEvent(st, c->events[li], 0));
+    if (cmp && cmp->pass == 1) {
+        CUDA_TRY(c, launch_compact_scan((const uint32_t *)c->ccnt.p, (uint64_t *)c->coff.p, segs,
+                                        (unsigned long long *)cmp->out->n_feasible, st));
+        c->stat_launches++;
+    }
     c->last_count_ptr = ctr + nl;
     if (n_lists_out) *n_lists_out = (int)total_ctas;
     return PARADL_OK;
@@ -1036,6 +1105,31 @@ extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *sp
     if (count == 0) return PARADL_OK;
     if (out->feasible_bits) CUDA_TRY(c, cudaMemsetAsync(out->feasible_bits, 0, sizeof(uint32_t) * ((count + 31) / 32), st));
     return run_sweep(c, P, first, count, 0, 1, true, 0, out, st, nullptr);
+}
+
+extern "C" paradl_status paradl_sweep_compact(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first,
+                                              uint64_t count, const paradl_compact_out *out, void *stream) {
+    paradl_status s = need_device(c);
+    if (s) return s;
+    if (!out || !out->idx || !out->n_feasible) return fail(c, PARADL_EINVAL, "null compact output");
+    const Plan *PP = nullptr;
+    s = plan_sweep(c, spec, &PP);
+    if (s) return s;
+    const Plan &P = *PP;
+    if (first > P.total || count > P.total - first) return fail(c, PARADL_ERANGE, "range outside the sweep (%llu configs)", (unsigned long long)P.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = upload(c, P, st);
+    if (s) return s;
+    if (count == 0) {
+        CUDA_TRY(c, cudaMemsetAsync(out->n_feasible, 0, sizeof(uint64_t), st));
+        return PARADL_OK;
+    }
+    // pass 1: feasible count per tile, then the exclusive scan over the tiles in index order;
+    // pass 2: the same tiles write their feasible configurations from the scanned offsets
+    const CompactCall p1{1, out}, p2{2, out};
+    s = run_sweep(c, P, first, count, 0, 1, true, 0, nullptr, st, nullptr, &p1);
+    if (s) return s;
+    return run_sweep(c, P, first, count, 0, 1, true, 0, nullptr, st, nullptr, &p2);
 }
 
 extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
@@ -1074,13 +1168,10 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
         const int64_t nb = (nlists + 15) / 16;
         CUDA_TRY(c, c->lists2.ensure(sizeof(paradl_hit) * nb * k));
         CUDA_TRY(c, c->nvalid2.ensure(sizeof(uint32_t) * nb));
-        if (!c->mdone.p) {
-            CUDA_TRY(c, c->mdone.ensure(sizeof(unsigned int)));
-            CUDA_TRY(c, cudaMemsetAsync(c->mdone.p, 0, sizeof(unsigned int), st));
-        }
         lv_out = (paradl_hit *)c->lists2.p;
         lv_nv = (uint32_t *)c->nvalid2.p;
-        lv_done = (unsigned int *)c->mdone.p;
+        // last-block ticket: the per-call counters block, zeroed before every sweep
+        lv_done = (unsigned int *)(c->last_count_ptr + 2);
     }
     CUDA_TRY(c, launch_merge((const paradl_hit *)c->lists.p, nlists, k, cnt, 1, d_hits,
                              (unsigned long long *)d_n_feasible, st, nlists ? c->last_count_ptr + 1 : nullptr, 0, 0,

@@ -1424,9 +1424,28 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         uint32_t alpha_i = L.d[D_ALPHA], beta_i = L.d[D_BETA];
         uint32_t carry = 0;
         bool have_carry = false;
+        // compact mode: pass 1 counts the tile's feasible configurations, pass 2 writes them
+        // from the tile's scanned offset (warp ballot + popc of the lanes below)
+        uint32_t c_tile = 0;
+        uint64_t c_pos = (DENSE && a.c_off) ? a.c_off[w.tile_base + tile] : 0;
 
         // emits one step (step index jj within the tile) for every lane
         auto emit_dense = [&](bool act, double t_it, bool feas, uint32_t jj) {
+            if (a.c_cnt) {
+                c_tile += __popc(__ballot_sync(full, act && feas));
+                return;
+            }
+            if (a.c_idx) {
+                const unsigned bb = __ballot_sync(full, act && feas);
+                const uint64_t pos = c_pos + __popc(bb & ((1u << lane) - 1u));
+                if (act && feas && pos < a.c_cap) {
+                    a.c_idx[pos] = g0 + lane + 32ull * jj;
+                    if (a.t_iter) a.t_iter[pos] = t_it;
+                    if (a.mem) a.mem[pos] = m.mem;
+                }
+                c_pos += __popc(bb);
+                return;
+            }
             const uint64_t o = g0 + lane + 32ull * jj - a.first;
             if (act) {
                 if (a.t_iter) a.t_iter[o] = t_it;
@@ -1652,6 +1671,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
             const uint64_t pos_end = g0 + 32ull * nsteps - a.first;
             atomicOr(&a.bits[pos_end >> 5], carry);
         }
+        if (DENSE && a.c_cnt && lane == 0) a.c_cnt[w.tile_base + tile] = c_tile;
     
 }
 
@@ -2259,6 +2279,287 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
     }
 }
 
+// ------------------------------------------------------------------ mode 3: COMB partitions, incremental
+// Lane-blocked pipeline / pd sweeps over combination-mode partitions (the cfg5 shape: ~6.3e8
+// partitions x S x p_d x alpha x beta), ring collectives, at most 2 alpha and 2 beta rows.
+//
+// Stage terms.  A lane walks consecutive partitions, and the
+// lexicographic successor mostly moves only the last cut c = c_{s-1}: stages 0..s-3 are then
+// unchanged, so their maxima `pre` (and the prefix values at a = c_{s-2}) are kept, and only
+// stage s-2 = rows (a, c] and the last stage (c, G] are formed from the prefix values at c --
+// seven shared-memory loads and exact int64 differences / maxima, whatever s is.  Any other
+// successor (an earlier cut moves, the stage count or a slower digit changes) recomputes
+// `pre` from the cut list; every term is an exact integer maximum, so the split composes to
+// the same StageT as stage_terms().
+//
+// Keys.  The fp64 trees are eval_partition's, operation for operation, with each subtree
+// formed at the loop level it depends on: per partition FB = D(maxF + maxB), U tau, D(delta
+// maxY), D(delta maxW); per S (4 per pass) comp = ((cseg FB) tau + U tau) (+inf when S > b or
+// the partition is infeasible) and the pipeline term P = pp_c (alpha + (bS D(delta maxY))
+// beta) for the <= 2 x 2 alpha/beta rows; per p_d value the GE term G = ge_c (alpha + ge_s
+// beta) with ge_s = D(delta maxW) / p_d (x 2^-k exactly for a power of two); per
+// configuration t = comp + G, t = t + P, key = t I.  The (b, stage count, S) and (b, stage
+// count, p_d) constants -- cseg, pp_c, b/S, ge_c, I = D/(b p_d), the tiers' alpha/beta -- come
+// from per-CTA tables built with the memo (build_memo).  With one alpha (beta) row the second
+// is a duplicate of the first: duplicate keys cannot change a minimum.
+//
+// Selection.  Only the smallest high word of the partition's keys is kept (key <= adm implies
+// hi(key) <= hi(adm) for non-negative doubles); a partition that may hold a candidate is
+// re-evaluated by eval_partition (offers, exact).  Memory feasibility is the integer
+// threshold memI <= mem_threshold(cap), exactly the fp64 compare (mem_threshold).  The feasible
+// count is separable: (#S <= b) x (#p_d with a tier) x n_LAB per feasible partition.
+struct __align__(16) CmbN {   // per stage count n: P2P tier alpha/beta rows, dims with a tier
+    double a0, a1, b0, b1;
+    int32_t ndok, ok, pad0, pad1;
+};
+struct __align__(16) CmbS {   // per (b, n, S): (n + S - 1)(b/S), 2 (n + S - 2) or 0, b/S, S <= b
+    double cseg, ppc, bS;
+    int32_t sok, pad;
+};
+struct __align__(16) CmbD {   // per (b, n, dims): ring GE coefficient (+inf: no tier), D/(b p_d),
+    double gc, I, a0, a1, b0, b1, scale;   // GE tier alpha/beta rows, 2^-k for p_d = 2^k (else 0)
+    int32_t pd, div;                       // div: p_d not a power of two -> IEEE division
+};
+static_assert(sizeof(CmbN) == 48 && sizeof(CmbS) == 32 && sizeof(CmbD) == 64, "comb table layout");
+
+// Per-lane stage state of tile_body_comb in shared memory (column per thread, int64):
+// pre = maxima over stages 0..s-3 and the prefix values at a = c_{s-2}; pre2 = maxima over
+// stages 0..s-4 and the prefix values at c_{s-3} (the "mid" successor, which moves c_{s-2},
+// rebuilds pre from pre2 plus one stage).  Maxima: F, B, U, W, memI, Y; prefixes: F, B, U, W, XY, BI.
+enum { LS_PRE = 0, LS_APRE = 6, LS_PRE2 = 12, LS_BPRE = 18, kLaneState = 24 };
+static_assert(kLaneStateBytes == kLaneState * 8u * kThreads, "lane state layout");
+
+template <int FAM>
+__device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                               uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
+                               int64_t *lstate) {
+    BlkCtx C = make_blk(w, smem, memo);
+    const View &v = C.v;
+    const SubHdr *S = v.S;
+    const ImgHdr *H = v.H;
+    const ModelHdr *M = v.M;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int G = M->G;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+    const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+    const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    const int64_t *bv = at<int64_t>(v.img, S->off_b);
+    const int64_t delta = H->delta;
+    const double INF = CUDART_INF;
+    const uint32_t ns1 = (uint32_t)S->s_max + 1, nS = C.nS, nD = C.nD;
+    const uint8_t *cb = reinterpret_cast<const uint8_t *>(memo) + w.cmb_off;
+    const CmbN *tabN = reinterpret_cast<const CmbN *>(cb);
+    const CmbS *tabS = reinterpret_cast<const CmbS *>(cb + ns1 * sizeof(CmbN));
+    const CmbD *tabD =
+        reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nS * sizeof(CmbS));
+    int64_t *ls = lstate + threadIdx.x;
+    const uint64_t nblk = (w.hi - w.lo) / C.Q;
+    const uint64_t c = w.steps;
+    const uint64_t blk0 = (tile * 32 + lane) * c;
+    const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
+    const uint32_t iters = __reduce_max_sync(full, (uint32_t)nmine);
+    Lane L;
+    int clast = 0, ns = 1;
+    int upd = 2;   // stage state to rebuild before the next partition: 0 none, 1 mid, 2 all
+    double cap_memo = CUDART_NAN;
+    int64_t mem_max = -1;
+    if (nmine) decode(v, w.lo + blk0 * C.Q, L, cuts, kThreads);
+    for (uint32_t it = 0; it < iters; it++) {
+        const bool act = it < nmine;
+        StageT st;
+        st.maxF = st.maxB = st.maxU = st.maxW = st.maxY = st.sumY = st.memI = 0;
+        int64_t b = 1;
+        if (act) {
+            b = bv[L.d[D_B]];
+            const int64_t twob = 2 * b;
+            if (upd) {
+                ns = L.ns;
+                if (ns >= 2) {
+                    // a = c_{s-2} (row 0 if s = 2), b2 = c_{s-3} (row 0 if s <= 3)
+                    const int a0 = ns >= 3 ? cuts[(ns - 3) * kThreads] : 0;
+                    const int b2 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
+                    StageT p2;
+                    if (upd == 2) {   // maxima over stages 0..s-4 and the prefix values at b2
+                        p2.maxF = p2.maxB = p2.maxU = p2.maxW = p2.maxY = p2.sumY = p2.memI = 0;
+                        if (ns >= 4) stage_span(v, cuts, kThreads, twob, ns, 0, ns - 3, 0, p2);
+                        ls[(LS_PRE2 + 0) * kThreads] = p2.maxF;
+                        ls[(LS_PRE2 + 1) * kThreads] = p2.maxB;
+                        ls[(LS_PRE2 + 2) * kThreads] = p2.maxU;
+                        ls[(LS_PRE2 + 3) * kThreads] = p2.maxW;
+                        ls[(LS_PRE2 + 4) * kThreads] = p2.memI;
+                        ls[(LS_PRE2 + 5) * kThreads] = p2.maxY;
+                        ls[(LS_BPRE + 0) * kThreads] = PF[b2];
+                        ls[(LS_BPRE + 1) * kThreads] = PB[b2];
+                        ls[(LS_BPRE + 2) * kThreads] = PU[b2];
+                        ls[(LS_BPRE + 3) * kThreads] = PW[b2];
+                        ls[(LS_BPRE + 4) * kThreads] = PX[b2];
+                        ls[(LS_BPRE + 5) * kThreads] = PI[b2];
+                    } else {
+                        p2.maxF = ls[(LS_PRE2 + 0) * kThreads];
+                        p2.maxB = ls[(LS_PRE2 + 1) * kThreads];
+                        p2.maxU = ls[(LS_PRE2 + 2) * kThreads];
+                        p2.maxW = ls[(LS_PRE2 + 3) * kThreads];
+                        p2.memI = ls[(LS_PRE2 + 4) * kThreads];
+                        p2.maxY = ls[(LS_PRE2 + 5) * kThreads];
+                    }
+                    // stage s-3 = rows (b2, a] (exists when s >= 3), folded into pre
+                    const int64_t eF = PF[a0], eB = PB[a0], eU = PU[a0], eW = PW[a0], eX = PX[a0], eI = PI[a0];
+                    if (ns >= 3) {
+                        const int64_t W3 = eW - ls[(LS_BPRE + 3) * kThreads];
+                        p2.maxF = max(p2.maxF, eF - ls[(LS_BPRE + 0) * kThreads]);
+                        p2.maxB = max(p2.maxB, eB - ls[(LS_BPRE + 1) * kThreads]);
+                        p2.maxU = max(p2.maxU, eU - ls[(LS_BPRE + 2) * kThreads]);
+                        p2.maxW = max(p2.maxW, W3);
+                        p2.memI = max(p2.memI, twob * (eX - ls[(LS_BPRE + 4) * kThreads]) + 2 * W3 +
+                                                   (eI - ls[(LS_BPRE + 5) * kThreads]));
+                        p2.maxY = max(p2.maxY, Y[a0 - 1]);
+                    }
+                    ls[(LS_PRE + 0) * kThreads] = p2.maxF;
+                    ls[(LS_PRE + 1) * kThreads] = p2.maxB;
+                    ls[(LS_PRE + 2) * kThreads] = p2.maxU;
+                    ls[(LS_PRE + 3) * kThreads] = p2.maxW;
+                    ls[(LS_PRE + 4) * kThreads] = p2.memI;
+                    ls[(LS_PRE + 5) * kThreads] = p2.maxY;
+                    ls[(LS_APRE + 0) * kThreads] = eF;
+                    ls[(LS_APRE + 1) * kThreads] = eB;
+                    ls[(LS_APRE + 2) * kThreads] = eU;
+                    ls[(LS_APRE + 3) * kThreads] = eW;
+                    ls[(LS_APRE + 4) * kThreads] = eX;
+                    ls[(LS_APRE + 5) * kThreads] = eI;
+                    clast = cuts[(ns - 2) * kThreads];
+                }
+                upd = 0;
+            }
+            if (ns == 1) {
+                st.maxF = PF[G] - PF[0];
+                st.maxB = PB[G] - PB[0];
+                st.maxU = PU[G] - PU[0];
+                st.maxW = PW[G] - PW[0];
+                st.memI = twob * (PX[G] - PX[0]) + 2 * (PW[G] - PW[0]) + (PI[G] - PI[0]);
+            } else {
+                // stage s-2 = rows (a, c], stage s-1 = rows (c, G]
+                const int64_t cF = PF[clast], cB = PB[clast], cU = PU[clast], cW = PW[clast], cX = PX[clast],
+                              cI = PI[clast], y = Y[clast - 1];
+                const int64_t W1 = cW - ls[(LS_APRE + 3) * kThreads], W2 = PW[G] - cW;
+                st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - ls[(LS_APRE + 0) * kThreads], PF[G] - cF));
+                st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - ls[(LS_APRE + 1) * kThreads], PB[G] - cB));
+                st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - ls[(LS_APRE + 2) * kThreads], PU[G] - cU));
+                st.maxW = max(ls[(LS_PRE + 3) * kThreads], max(W1, W2));
+                st.memI = max(ls[(LS_PRE + 4) * kThreads],
+                              max(twob * (cX - ls[(LS_APRE + 4) * kThreads]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * kThreads]),
+                                  twob * (PX[G] - cX) + 2 * W2 + (PI[G] - cI)));
+                st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
+            }
+        }
+        // ---- keys of the partition's S x dims x Ls x alpha x beta block
+        double FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, part_inf = INF;
+        double at0 = 0.0, at1 = 0.0, bt0 = 0.0, bt1 = 0.0;
+        uint32_t ndok = 0, bi = 0;
+        if (act) {
+            const double cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
+            const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
+            if (R != C.R_memo) {
+                C.R_memo = R;
+                C.tau = ddiv_rare(1.0, R);
+            }
+            if (!(cap == cap_memo)) {
+                cap_memo = cap;
+                mem_max = mem_threshold(H, cap);
+            }
+            bi = L.d[D_B];
+            const CmbN tn = tabN[ns];
+            at0 = tn.a0, at1 = tn.a1, bt0 = tn.b0, bt1 = tn.b1;
+            ndok = (uint32_t)tn.ndok;
+            part_inf = (tn.ok && st.memI <= mem_max) ? 0.0 : INF;
+            FBs = i2d(st.maxF + st.maxB);
+            Utau = dmul(i2d(st.maxU), C.tau);
+            dmaxY = i2d(delta * st.maxY);
+            if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
+        }
+        const double tau = C.tau;
+        const CmbS *srow = tabS + ((size_t)bi * ns1 + ns) * nS;
+        const CmbD *drow = tabD + ((size_t)bi * ns1 + ns) * nD;
+        int hmin = 0x7fffffff;
+        uint32_t nSok = 0;
+        for (uint32_t iS0 = 0; iS0 < nS; iS0 += kSB) {
+            double comp[kSB], P[kSB][4];
+#pragma unroll
+            for (int u = 0; u < kSB; u++) {
+                const uint32_t iS = iS0 + u < nS ? iS0 + u : nS - 1;
+                const CmbS q = srow[iS];
+                const bool sok = act && q.sok && iS0 + u < nS;
+                nSok += sok ? 1u : 0u;
+                comp[u] = dadd(dadd(dmul(dmul(q.cseg, FBs), tau), Utau), sok ? part_inf : INF);
+                const double pps = dmul(q.bS, dmaxY);
+                const double x0 = dmul(pps, bt0), x1 = dmul(pps, bt1);
+                P[u][0] = dmul(q.ppc, dadd(at0, x0));
+                P[u][1] = dmul(q.ppc, dadd(at0, x1));
+                P[u][2] = dmul(q.ppc, dadd(at1, x0));
+                P[u][3] = dmul(q.ppc, dadd(at1, x1));
+            }
+#pragma unroll 1
+            for (uint32_t iD = 0; iD < nD; iD++) {
+                const CmbD d = drow[iD];
+                double Gq[4] = {0.0, 0.0, 0.0, 0.0};
+                if (FAM == PARADL_PD) {
+                    const double gs = d.div ? ddiv_rare(mW, i2d(d.pd)) : dmul(mW, d.scale);
+                    const double g0 = dmul(gs, d.b0), g1 = dmul(gs, d.b1);
+                    Gq[0] = dmul(d.gc, dadd(d.a0, g0));
+                    Gq[1] = dmul(d.gc, dadd(d.a0, g1));
+                    Gq[2] = dmul(d.gc, dadd(d.a1, g0));
+                    Gq[3] = dmul(d.gc, dadd(d.a1, g1));
+                }
+#pragma unroll
+                for (int u = 0; u < kSB; u++) {
+                    int h[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const double t = FAM == PARADL_PD ? dadd(dadd(comp[u], Gq[q]), P[u][q]) : dadd(comp[u], P[u][q]);
+                        h[q] = __double2hiint(dmul(t, d.I));
+                    }
+                    hmin = min(hmin, min(min(h[0], h[1]), min(h[2], h[3])));
+                }
+            }
+        }
+        if (act && part_inf == 0.0) cnt += (unsigned long long)nSok * ndok * C.nLAB;
+        const bool maybe = act && hmin <= __double2hiint(tk.adm);
+        if (__any_sync(full, maybe)) {
+            const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
+            eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
+        }
+        tk.refresh();
+        if (it + 1 < nmine) {
+            if (ns >= 2 && clast < G - 1) {   // lexicographic successor moves only the last cut
+                clast++;
+                L.part++;
+            } else if (ns >= 3 && L.part + 1 < S->part_n) {
+                // an earlier cut moves (same stage count: the last cut is at its maximum, so
+                // the successor is inside this stage-count block unless every cut is)
+                cuts[(ns - 2) * kThreads] = (uint16_t)clast;
+                const int c3 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
+                succ_comb(v, L, cuts, kThreads);
+                L.part++;
+                upd = (L.ns == ns && (ns < 4 || cuts[(ns - 4) * kThreads] == c3)) ? 1 : 2;
+            } else {
+                // a successor that moves c_{s-2} (same s, same slower digits, c_{s-3} kept)
+                // rebuilds pre from pre2 and one stage; anything else rebuilds both
+                if (ns >= 2) cuts[(ns - 2) * kThreads] = (uint16_t)clast;
+                const int c3 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
+                const uint32_t d0 = L.d[D_B], d1 = L.d[D_FLOPS], d2 = L.d[D_CAP];
+                advance(w, v, L, cuts, kThreads);
+                const bool mid = ns >= 3 && L.ns == ns && L.d[D_B] == d0 && L.d[D_FLOPS] == d1 && L.d[D_CAP] == d2 &&
+                                 (ns < 4 || cuts[(ns - 4) * kThreads] == c3);
+                upd = mid ? 1 : 2;
+            }
+        }
+    }
+}
+
 // Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
 // with the same fp64 operations compute_mid uses, and the low-bit stage tables of mode 2.
 __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base, LowE *low_base) {
@@ -2302,7 +2603,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
         const int32_t *Sv = at<int32_t>(v.img, S->off_S);
         const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
         const uint32_t nrow = S->radix[D_B] * (nS + nD);
-        if (w.family == PARADL_PD && w.mode == 1) {
+        if (w.family == PARADL_PD && (w.mode == 1 || w.mode == 3)) {
             // ring GE coefficient and tier per (stage count s, dims value): make_ar's ring
             // branch, ge_c = 2 (p_d - 1) (0 when p_d = 1), +inf when s p_d exceeds every tier
             const uint32_t nDp = nD + 1;
@@ -2329,6 +2630,65 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                     gc[e] = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
                     gt[e] = max(tp, 0);
                 }
+            }
+        }
+        if (w.mode == 3) {
+            // mode-3 tables (tile_body_comb): per stage count n the P2P tier's alpha/beta rows,
+            // per (b, n, S) and (b, n, dims) the constants of eval_partition's trees
+            const uint32_t ns1 = (uint32_t)S->s_max + 1, nb = S->radix[D_B];
+            const uint32_t nA = S->radix[D_ALPHA], nBt = S->radix[D_BETA];
+            const int NT = v.H->n_tiers;
+            const double *al = at<double>(v.img, S->off_alpha), *be = at<double>(v.img, S->off_beta);
+            uint8_t *cb = reinterpret_cast<uint8_t *>(memo_base) + w.cmb_off;
+            CmbN *tn = reinterpret_cast<CmbN *>(cb);
+            CmbS *ts = reinterpret_cast<CmbS *>(cb + ns1 * sizeof(CmbN));
+            CmbD *td = reinterpret_cast<CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)nb * ns1 * nS * sizeof(CmbS));
+            const uint32_t ia1 = nA > 1 ? 1 : 0, ib1 = nBt > 1 ? 1 : 0;
+            for (uint32_t n = threadIdx.x; n < ns1; n += blockDim.x) {
+                const int t = n >= 1 ? tier_of(v.H, n) : -1;
+                const int tt = max(t, 0);
+                CmbN q;
+                q.a0 = al[tt];
+                q.a1 = al[ia1 * NT + tt];
+                q.b0 = be[tt];
+                q.b1 = be[ib1 * NT + tt];
+                int ok = 0;
+                for (uint32_t j = 0; j < nD; j++)
+                    ok += w.family == PARADL_PD ? tier_of(v.H, (int64_t)n * dmv[4 * j]) >= 0 : 1;
+                q.ndok = ok;
+                q.ok = t >= 0;
+                q.pad0 = q.pad1 = 0;
+                tn[n] = q;
+            }
+            for (uint32_t e = threadIdx.x; e < nb * ns1 * nS; e += blockDim.x) {
+                const uint32_t ib = e / (ns1 * nS), n = (e / nS) % ns1, j = e % nS;
+                const int64_t b = bv[ib], Sg = Sv[j];
+                CmbS q;
+                q.bS = ddiv(i2d(b), i2d(Sg));
+                q.cseg = dmul(i2d((int64_t)n + Sg - 1), q.bS);
+                q.ppc = n > 1 ? i2d(2 * ((int64_t)n + Sg - 2)) : 0.0;
+                q.sok = Sg >= 1 && Sg <= b;
+                q.pad = 0;
+                ts[e] = q;
+            }
+            for (uint32_t e = threadIdx.x; e < nb * ns1 * nD; e += blockDim.x) {
+                const uint32_t ib = e / (ns1 * nD), n = (e / nD) % ns1, j = e % nD;
+                const int64_t b = bv[ib];
+                const int64_t pd = w.family == PARADL_PD ? dmv[4 * j] : 1;
+                const int tp = tier_of(v.H, (int64_t)n * pd);
+                const int tt = max(tp, 0);
+                CmbD q;
+                q.I = ddiv(i2d(v.M->D), i2d(b * pd));
+                q.gc = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
+                q.a0 = al[tt];
+                q.a1 = al[ia1 * NT + tt];
+                q.b0 = be[tt];
+                q.b1 = be[ib1 * NT + tt];
+                const bool pow2 = pd > 0 && (pd & (pd - 1)) == 0;
+                q.scale = pow2 ? __longlong_as_double((long long)(1023 - (63 - __clzll(pd))) << 52) : 0.0;
+                q.pd = (int32_t)pd;
+                q.div = !pow2;
+                td[e] = q;
             }
         }
         if (w.mode == 2 && (w.flags & kWorkMaskD)) {
@@ -2446,6 +2806,11 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
         const WorkItem &w = a.work[wi];
         if (BLK == 1)
             tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, dtab);
+        else if (BLK == 3) {
+            if (FAM == PARADL_PIPELINE || FAM == PARADL_PD)
+                tile_body_comb<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
+                                    reinterpret_cast<int64_t *>(dtab));
+        }
         else if (BLK == 2) {
             if (FAM == PARADL_PIPELINE && (w.flags & kWorkMaskD))
                 tile_body_mask_d<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
@@ -2992,7 +3357,7 @@ __global__ void __launch_bounds__(256) struct_table_kernel(const uint8_t *img, u
     extern __shared__ __align__(128) uint8_t simg[];
     __shared__ uint64_t mbar;
     if (job.ctr && blockIdx.x == 0)   // replaces two memsets ahead of the sweep launches
-        for (int i = threadIdx.x; i <= job.n_ctr; i += blockDim.x) job.ctr[i] = i < job.n_ctr ? 0ull : ~0ull;
+        for (int i = threadIdx.x; i <= job.n_ctr + 1; i += blockDim.x) job.ctr[i] = i == job.n_ctr ? ~0ull : 0ull;
     stage_image(simg, img, img_bytes, &mbar);
     const View v = make_view(simg, job.sub);
     const SubHdr *S = v.S;
@@ -3079,6 +3444,52 @@ cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ compact mode: tile offsets
+// Exclusive scan of the per-tile feasible counts in ascending index order (segments of the
+// launches' tile spaces), one block: off[slot] = feasible configurations before the tile.
+__global__ void __launch_bounds__(1024) compact_scan_kernel(const uint32_t *cnt, uint64_t *off,
+                                                            const __grid_constant__ CompactSegs segs,
+                                                            unsigned long long *total) {
+    __shared__ unsigned long long wsum[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long run = 0;
+    for (int g = 0; g < segs.n; g++) {
+        for (uint64_t i0 = 0; i0 < segs.cnt[g]; i0 += blockDim.x) {
+            const uint64_t i = i0 + threadIdx.x;
+            const unsigned long long v = i < segs.cnt[g] ? cnt[segs.slot[g] + i] : 0ull;
+            unsigned long long x = v;   // inclusive warp scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                unsigned long long z = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0ull;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+                    if (lane >= o) z += y;
+                }
+                wsum[lane] = z;   // inclusive prefix over warps
+            }
+            __syncthreads();
+            const unsigned long long before = (warp ? wsum[warp - 1] : 0ull) + x - v;
+            if (i < segs.cnt[g]) off[segs.slot[g] + i] = run + before;
+            run += wsum[(blockDim.x >> 5) - 1];
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) *total = run;
+}
+
+cudaError_t launch_compact_scan(const uint32_t *cnt, uint64_t *off, const CompactSegs &segs,
+                                unsigned long long *total, cudaStream_t st) {
+    compact_scan_kernel<<<1, 1024, 0, st>>>(cnt, off, segs, total);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ launchers
 size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
@@ -3087,11 +3498,15 @@ static void *sweep_fn(int family, bool dense, int blk) {
         if (dense) return nullptr;
         switch (family) {
         case PARADL_PIPELINE:
-            return blk == 1 ? (void *)sweep_kernel<PARADL_PIPELINE, false, 1> : (void *)sweep_kernel<PARADL_PIPELINE, false, 2>;
+            return blk == 1   ? (void *)sweep_kernel<PARADL_PIPELINE, false, 1>
+                   : blk == 3 ? (void *)sweep_kernel<PARADL_PIPELINE, false, 3>
+                              : (void *)sweep_kernel<PARADL_PIPELINE, false, 2>;
         case PARADL_LAYERPURE:
             return blk == 1 ? (void *)sweep_kernel<PARADL_LAYERPURE, false, 1> : (void *)sweep_kernel<PARADL_LAYERPURE, false, 2>;
         case PARADL_PD:
-            return blk == 1 ? (void *)sweep_kernel<PARADL_PD, false, 1> : (void *)sweep_kernel<PARADL_PD, false, 2>;
+            return blk == 1   ? (void *)sweep_kernel<PARADL_PD, false, 1>
+                   : blk == 3 ? (void *)sweep_kernel<PARADL_PD, false, 3>
+                              : (void *)sweep_kernel<PARADL_PD, false, 2>;
         default: return nullptr;
         }
     }

@@ -27,6 +27,8 @@ constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 constexpr int kGpMax = PARADL_GPIPE_MAX_STAGES;
+// mode-3 (COMB, incremental stage terms) per-lane stage state: 24 int64 per thread, column layout
+constexpr uint32_t kLaneStateBytes = 24u * 8u * kThreads;
 // GPIPE per-lane stage table in shared memory: 4 doubles (f, g, m, u) per stage, column per thread
 constexpr uint32_t kGpipeTabBytes = 4u * kGpMax * 8u * kThreads;
 
@@ -95,12 +97,15 @@ struct WorkItem {
     uint64_t lo, hi, n_tiles, tile_base;
     uint32_t inc[kDigits];         // mixed-radix digits of the lane stride (32 configs, or 1 partition)
     int32_t mode;                  // 0: lane-strided (lanes = 32 consecutive configs); 1: lane-blocked
-                                   // (pipeline families: each lane owns whole partitions, [lo,hi) aligned)
+                                   // (pipeline families: each lane owns whole partitions, [lo,hi) aligned);
+                                   // 2: 256-mask blocks (MASK); 3: lane-blocked COMB, incremental stage terms
     uint64_t inc_part;
     const HaloEntry *halo;         // spatial / ds: [n_dims][n_Ls] table (device global), else null
     uint32_t memo_off, memo_n;     // mode 1/2: smem table [n_b][n_S + n_dims] of b/S and D/(b*p_d)
     uint32_t low_off, flags;       // mode 2: index of its [n_b][256] low-bit stage table (LowE units);
                                    // flags: kWorkMaskD = screened pipeline masks, stage terms as exact doubles
+    uint32_t cmb_off, pad_c;       // mode 3: byte offset (from the memo base) of its comb tables
+                                   // [CmbN x (s_max+1)][CmbS x n_b(s_max+1)n_S][CmbD x n_b(s_max+1)n_dims]
     const struct PipeRec *stab;    // mode 0 pipeline, reduce: structure table (device global), else null
     uint64_t stab_lo;              // structure index of stab[0] within the sub-sweep
 };
@@ -120,8 +125,8 @@ struct StructJob {
     int32_t sub, pad;
     uint64_t s_lo, n;              // structures [s_lo, s_lo + n) of sub-sweep `sub`
     PipeRec *out;
-    unsigned long long *ctr;       // non-null: zero ctr[0, n_ctr) and set ctr[n_ctr] = ~0 (the
-    int32_t n_ctr, pad2;           // sweep's tile counters, count and admission bound) first
+    unsigned long long *ctr;       // non-null: zero ctr[0, n_ctr), set ctr[n_ctr] = ~0 and zero
+    int32_t n_ctr, pad2;           // ctr[n_ctr + 1] (tile counters, count, admission bound, merge ticket)
     // sharded calls: only structures overlapping this shard's tiles are computed (tile T
     // covers local configs [w_lo + (T - tile_base) ts, +ts); T % n_shards == shard)
     uint64_t w_lo, w_hi, ts, tile_base;
@@ -149,7 +154,22 @@ struct LaunchArgs {
     double *mem;
     uint32_t *bits;
     uint8_t *reason;
+    // compact mode (paradl_sweep_compact): pass 1 writes the feasible count of every tile to
+    // c_cnt[T]; pass 2 writes tile T's feasible configurations from offset c_off[T] on
+    uint32_t *c_cnt;
+    const uint64_t *c_off;
+    uint64_t *c_idx;
+    uint64_t c_cap;
     WorkItem work[kMaxWork];
+};
+
+// Tile segments of a compact sweep in ascending index order: slots [slot, slot + n) of the
+// per-launch tile-count arrays (launch tile spaces concatenated)
+constexpr int kMaxSegs = 256;
+struct CompactSegs {
+    int32_t n, pad;
+    uint64_t slot[kMaxSegs];
+    uint64_t cnt[kMaxSegs];
 };
 
 struct HaloJob {
@@ -177,6 +197,8 @@ cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          unsigned long long *bound_out = nullptr, const uint32_t *nvalid = nullptr,
                          paradl_hit *lv_out = nullptr, uint32_t *lv_nvalid = nullptr, unsigned int *lv_done = nullptr);
 cudaError_t launch_halo_tables(const HaloJobs &jobs, cudaStream_t st);
+cudaError_t launch_compact_scan(const uint32_t *cnt, uint64_t *off, const CompactSegs &segs,
+                                unsigned long long *total, cudaStream_t st);
 cudaError_t launch_struct_table(const uint8_t *img, uint32_t img_bytes, const StructJob &job, uint64_t unit_len,
                                 cudaStream_t st);
 cudaError_t launch_fp64_bench(int n_sm, int iters, double *d_sink, cudaStream_t st, int *threads_out);

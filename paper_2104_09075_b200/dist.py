@@ -8,6 +8,8 @@ to the 1-GPU result.  A hit record is two int64 words: (idx, key bits of the fp6
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.distributed as dist
 
@@ -33,16 +35,25 @@ def sharded_topk(ctx, spec, first: int, count: int, k: int, out_hits: torch.Tens
     """One multi-GPU top-k step on the current device: shard -> one all_gather -> device merge.
     my_rec: int64 [k + 1, 2] record (k hits, then the count in row k, column 0); out_hits
     [k, 2] and out_count [1] int64 on the ctx's device.  Returns (out_hits, out_count, stats)
-    with this rank's H2D bytes and kernel launches."""
+    with this rank's H2D bytes and kernel launches.
+
+    Stream order: the sweep, the collective and the merge all run on `stream` (default: the
+    caller's current stream).  The collective is issued under `torch.cuda.stream(stream)`,
+    so NCCL waits for the sweep that writes my_rec and the merge waits for the gather, even
+    when `stream` is not torch's current stream."""
     ws = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    on_gpu = my_rec.is_cuda
+    if stream is None and on_gpu:
+        stream = torch.cuda.current_stream(my_rec.device)
     ctx.topk_async(spec, first, count, rank, ws, k, my_rec.data_ptr(), my_rec[k].data_ptr(), stream=stream)
     stats = {"h2d": ctx.stat(0), "launches": ctx.stat(2) + 1}
-    recs = torch.empty((ws, k + 1, 2), dtype=torch.int64, device=my_rec.device)
-    if dist.get_backend(group) == "gloo":
-        dist.all_gather(list(recs.unbind(0)), my_rec.contiguous(), group=group)
-    else:
-        dist.all_gather_into_tensor(recs.view(ws, -1), my_rec.reshape(-1).contiguous(), group=group)
+    with torch.cuda.stream(stream) if on_gpu else contextlib.nullcontext():
+        recs = torch.empty((ws, k + 1, 2), dtype=torch.int64, device=my_rec.device)
+        if dist.get_backend(group) == "gloo":
+            dist.all_gather(list(recs.unbind(0)), my_rec.contiguous(), group=group)
+        else:
+            dist.all_gather_into_tensor(recs.view(ws, -1), my_rec.reshape(-1).contiguous(), group=group)
     ctx.merge_records(recs.data_ptr(), ws, k, out_hits.data_ptr(), out_count.data_ptr(), stream=stream)
     return out_hits, out_count, stats
 

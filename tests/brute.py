@@ -331,6 +331,41 @@ def ring_allreduce_sim(p, m, alpha, beta):
     return t, acc
 
 
+def concurrent_rings_sim(group_bytes, p, alpha, beta):
+    """pd gradient exchange (Q17): one ring Allreduce per pipeline stage, each among
+    the p replicas of that stage, all stages at once over disjoint PE groups.  A discrete-
+    event run: every group owns its PEs and links, so a step of group g starts when that
+    group's previous step ends; a step sends one chunk per PE (reduce-scatter, then
+    allgather) and the reduced buffers are checked.  Returns the makespan (exact rationals)."""
+    if p == 1:
+        return Fr(0)
+    clock = [Fr(0)] * len(group_bytes)
+    accs = []
+    for g, m in enumerate(group_bytes):
+        seg = Fr(m, p)
+        acc = [[(i + 1) * 1000 + c + 7 * g for c in range(p)] for i in range(p)]
+        events = []
+        for step in range(p - 1):
+            events.append(("rs", step))
+        for step in range(p - 1):
+            events.append(("ag", step))
+        for kind, step in events:            # interleaving across groups cannot matter:
+            if kind == "rs":                 # links and PEs are disjoint
+                sends = [(i, (i - step) % p, acc[i][(i - step) % p]) for i in range(p)]
+                for i, c, v in sends:
+                    acc[(i + 1) % p][c] += v
+            else:
+                sends = [(i, (i + 1 - step) % p, acc[i][(i + 1 - step) % p]) for i in range(p)]
+                for i, c, v in sends:
+                    acc[(i + 1) % p][c] = v
+            clock[g] += alpha + seg * beta
+        accs.append(acc)
+    for g, acc in enumerate(accs):
+        col = [sum((i + 1) * 1000 + c + 7 * g for i in range(p)) for c in range(p)]
+        assert all(row == col for row in acc)
+    return max(clock)
+
+
 def ring_allgather_sim(p, m_seg, alpha, beta):
     if p == 1:
         return Fr(0)
@@ -392,17 +427,6 @@ def buffer_bytes(sweep, cfg):
     elif fam in (W.SPATIAL, W.DS):
         p2 = d1 * d2 * d3
         tot = sum(layer_bufs(r, b * p1, p1 * p2, 1) for r in L)     # spatial shard of the group batch
-    elif fam == W.DATA_LW:
-        # data parallelism, one Allreduce per weighted layer, ring or tree per message (Q37)
-        p = p1
-        B = b * p
-        comp = comp_row(B, p, 1)
-        t = tier(p)
-        ge = inf if t is None else sum(ar_exact(sys, p, Fr(dl * r.w), Fr(dl * r.w, p), A[t], Bt[t])
-                                       for r in L if r.w > 0)
-        mem = mem_row(B, p, 1)
-        if p > B:
-            reason |= R_SCALING
     elif fam == W.SPATIAL_AG:
         p2 = d1 * d2 * d3
         Lp = min(cfg["Ls"], len(L))

@@ -483,3 +483,163 @@ def test_pipeline_ab_blocks(dev, oracle_mod, kw):
         a = rng.randrange(n // 2)
         c = rng.randrange(n // 4, n - a)
         check_topk(ctx, spec, osw, a, c, 32)
+
+
+# ------------------------------------------------------------------ headline-path parity (round 2)
+def test_pipeline_structure_table_vs_oracle(dev, oracle_mod):
+    """The pipeline path behind the headline sweeps' dominant sub-sweep: lane-strided work
+    items of >= 2^22 configurations read their structure terms from the structure table
+    (struct_table_kernel).  Whole sub-sweep top-64 / argmin and count, and ragged windows of
+    >= 2^22 configurations, against the oracle (Table 2 Layer row)."""
+    sw = W.config2(n_alpha=8, n_beta=64, b_list=[2, 32], pipe_smax=3)
+    sw.subs = [s for s in sw.subs if s.family == W.PIPELINE]
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    assert ctx.sweep_size(spec) == n and n >= (1 << 22)
+    check_topk(ctx, spec, osw, 0, n, 64)
+    check_topk(ctx, spec, osw, 0, n, 1)
+    (best, key), nf = ctx.argmin(spec)
+    ohits, onf = osw.topk(0, n, 1)
+    assert best == ohits[0][0] and nf == onf
+    for a, c in [(12345, (1 << 22) + 777), (n - (1 << 22) - 31, (1 << 22) + 31), (3, n - 5)]:
+        check_topk(ctx, spec, osw, a, c, 64)
+
+
+def test_sharded_large_vs_oracle(dev, oracle_mod):
+    """The 60M-configuration cfg2 shape (structure table built per shard) sharded 4 ways and
+    merged on the device, against the oracle's top-64 and count of the same range."""
+    sw = W.config2(n_alpha=64, n_beta=64, b_list=[8, 64, 256], pipe_smax=3)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    k, ns = 64, 4
+    ohits, onf = osw.topk(0, n, k)
+    recs = torch.zeros((ns, k + 1, 2), dtype=torch.int64, device=dev)
+    for s in range(ns):
+        ctx.topk_async(spec, 0, n, s, ns, k, recs[s].data_ptr(), recs[s, k].data_ptr(),
+                       stream=torch.cuda.current_stream())
+    out = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    ctx.merge_records(recs.data_ptr(), ns, k, out.data_ptr(), cnt.data_ptr(), stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert [int(v) for v in o[:, 0].astype(np.uint64)] == [h[0] for h in ohits]
+    assert o[:, 1].view(np.float64).tolist() == [h[1] for h in ohits]
+    assert int(cnt.item()) == onf
+
+
+def test_config4_full_sweep_vs_oracle(dev, oracle_mod):
+    """cfg4 (CosmoFlow 128^3 / 512^3 spatial + ds, 1.58e8 configurations) in full: the bench's
+    launch (whole-sweep top-64 + count) against the oracle's whole-sweep reduction."""
+    sw = W.config4()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    hits, nf = ctx.topk(spec, 64, 0, n)
+    ohits, onf = osw.topk(0, n, 64)
+    assert nf == onf
+    assert [h[0] for h in hits] == [h[0] for h in ohits]
+    assert [h[1] for h in hits] == [h[1] for h in ohits]
+
+
+def _golden_full(cfg):
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", f"full_cfg{cfg}.json")
+    if not os.path.exists(p):
+        pytest.skip(f"no whole-sweep oracle golden for cfg{cfg} (tools/golden_full.py {cfg})")
+    return json.load(open(p))
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_full_sweep_vs_oracle_golden(dev, cfg):
+    """Whole BASELINE sweep exactly as bench.py launches it (one top-64 + count call over
+    [0, N)) against the oracle's whole-sweep top-64 and count, written offline by
+    tools/golden_full.py from oracle/ alone."""
+    g = _golden_full(cfg)
+    sw = W.CONFIGS[cfg]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    n = ctx.sweep_size(spec)
+    assert n == g["configs"] and sw.name == g["workload"]
+    hits, nf = ctx.topk(spec, 64, 0, n)
+    assert nf == g["n_feasible"]
+    assert [h[0] for h in hits[:len(g["hits"])]] == [i for i, _ in g["hits"]]
+    assert [h[1] for h in hits[:len(g["hits"])]] == [float.fromhex(k) for _, k in g["hits"]]
+
+
+# ------------------------------------------------------------------ a9 compact mode
+def gpu_compact(ctx, spec, first, count, dev, capacity=None):
+    cap = count if capacity is None else capacity
+    idx = torch.empty(max(1, cap), dtype=torch.int64, device=dev)
+    t = torch.empty(max(1, cap), dtype=torch.float64, device=dev)
+    m = torch.empty(max(1, cap), dtype=torch.float64, device=dev)
+    nf = torch.zeros(1, dtype=torch.int64, device=dev)
+    ctx.sweep_compact(spec, first, count, idx.data_ptr(), cap, nf.data_ptr(), t.data_ptr(), m.data_ptr(),
+                      stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    n = int(nf.item())
+    k = min(n, cap)
+    return n, idx[:k].cpu().numpy().view(np.uint64), t[:k].cpu().numpy(), m[:k].cpu().numpy()
+
+
+def check_compact(ctx, spec, osw, first, count, dev):
+    """Compact output == the oracle's dense output filtered by its feasibility bits, in index order."""
+    n, idx, t, m = gpu_compact(ctx, spec, first, count, dev)
+    ot, om, obits, ors = osw.dense(first, count)
+    feas = np.nonzero(ors == 0)[0]
+    assert n == len(feas)
+    assert np.array_equal(idx, (feas + first).astype(np.uint64))
+    assert np.array_equal(t, ot[feas]) and np.array_equal(m, om[feas])
+    return n
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_compact_random_corpus(dev, oracle_mod, seed):
+    """Row a9 compact mode on random corpora (all families): whole range and ragged windows."""
+    sw = corpus.random_sweep(seed)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    check_compact(ctx, spec, osw, 0, n, dev)
+    rng = random.Random(seed)
+    for _ in range(3):
+        a = rng.randrange(n)
+        c = rng.randrange(n - a + 1)
+        check_compact(ctx, spec, osw, a, c, dev)
+
+
+@pytest.mark.parametrize("cfg,kw", [(2, dict(n_alpha=3, n_beta=5, b_list=[1, 7, 64, 256], pipe_smax=3)),
+                                    (4, dict(n_alpha=2, n_beta=3))])
+def test_compact_reduced_configs_and_capacity(dev, oracle_mod, cfg, kw):
+    """Compact mode on reduced BASELINE configs (many tiles, several launches), plus a capacity
+    smaller than the feasible count: the first `capacity` entries, and the full count."""
+    sw = W.CONFIGS[cfg](**kw)
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    nf = check_compact(ctx, spec, osw, 0, n, dev)
+    cap = max(1, nf // 3)
+    n2, idx, t, _ = gpu_compact(ctx, spec, 0, n, dev, capacity=cap)
+    ot, _, _, ors = osw.dense(0, n)
+    feas = np.nonzero(ors == 0)[0][:cap]
+    assert n2 == nf and np.array_equal(idx, feas.astype(np.uint64)) and np.array_equal(t, ot[feas])
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_compact_full_size_windows(dev, oracle_mod, cfg):
+    """Compact mode at full BASELINE sizes: windows at random offsets against the oracle."""
+    sw = W.CONFIGS[cfg]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    rng = random.Random(300 + cfg)
+    for a in [0, n - 5000] + [rng.randrange(n - 5000) for _ in range(6)]:
+        check_compact(ctx, spec, osw, a, rng.randrange(1000, 5000), dev)

@@ -250,6 +250,27 @@ def test_pipeline_examples(oracle_mod):
     assert pr.t_p2p == e["expect"]
 
 
+@pytest.mark.parametrize("pd", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("ws", [(1000, 7, 123457), (64, 64), (5, 999999, 3, 17)])
+def test_pd_ge_equals_concurrent_rings(oracle_mod, pd, ws):
+    """pd gradient exchange for p_d > 1 (Q17): the s stages' Allreduces run at once,
+    each among the p_d replicas of its stage on disjoint PEs, so the phase is the slowest
+    group's ring -- an explicit concurrent ring simulation (tests/brute.py), not the
+    AR(p_d, delta max W_i) formula, fixes the value.  One row per stage (s = G)."""
+    a, b = 3e-6, 1.0 / 7e9
+    rows = [toys.row(w=w, fw=1, bw=1, y=1) for w in ws]
+    m = toys.model(rows)
+    G = len(rows)
+    pr = _one(oracle_mod, m, toys.system(alpha=a, beta=b, delta=4),
+              W.SubSweep(W.PD, b=[8], S=[1], dims=[(pd, 1, 1, 1)], part_mode=W.PART_COMB, s_min=G, s_max=G))
+    want = brute.concurrent_rings_sim([4 * w for w in ws], pd, Fr(a), Fr(b))
+    assert _rel(pr.t_ge, want) <= 4e-16
+    assert pr.p == G * pd and pr.B == 8 * pd
+    pr1 = _one(oracle_mod, m, toys.system(alpha=a, beta=b, delta=4),
+               W.SubSweep(W.PD, b=[8], S=[1], dims=[(1, 1, 1, 1)], part_mode=W.PART_COMB, s_min=G, s_max=G))
+    assert pr1.t_ge == 0.0
+
+
 def test_partition_balanced_example(oracle_mod):
     e = EX["partition_balanced"]
     m = toys.model([toys.row(fw=c, bw=0) for c in e["costs"]], D=1)
