@@ -58,9 +58,24 @@ static int64_t ceil_log2(int64_t n)
 /* ------------------------------------------------------------------ spec helpers */
 static int64_t nz(int32_t n) { return n > 0 ? n : 1; }
 
+static int64_t comm_rows(const or_model *m)
+{
+    int64_t n = 0;
+    for (int64_t l = 0; l < m->G; l++) n += (m->rows[l].flags & OR_FLAG_COMM) != 0;
+    return n;
+}
+
 static int part_count(const or_model *m, const or_sub *s, uint64_t *out)
 {
     int fam = s->family;
+    if (fam == OR_LAYERWISE) {
+        /* one bit per COMM row: 1 = filter-parallel, 0 = data-parallel (Q39) */
+        if (s->part_mode != OR_PART_MASK) FAIL(E_INVAL, "layerwise needs the mask partition mode");
+        int64_t nc = comm_rows(m);
+        if (nc > 62) FAIL(E_INVAL, "layerwise needs at most 62 COMM rows");
+        *out = (uint64_t)1 << nc;
+        return 0;
+    }
     int is_pipe = (fam == OR_PIPELINE || fam == OR_LAYERPURE || fam == OR_PD || fam == OR_GPIPE);
     if (!is_pipe) {
         if (s->part_mode != OR_PART_NONE) FAIL(E_INVAL, "partition mode on a non-pipeline family");
@@ -191,7 +206,7 @@ int or_decode(const or_model *models, int n_models, const or_system *sys,
     }
     /* stage partition (groups g_i, P:519 footnote) */
     int64_t G = m->G;
-    if (s->part_mode == OR_PART_NONE) {
+    if (s->part_mode == OR_PART_NONE || s->family == OR_LAYERWISE) {
         c->n_stages = 1;
         c->stage_end[0] = (int32_t)G;
     } else if (s->part_mode == OR_PART_MASK) {
@@ -568,6 +583,83 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (p > B) reason |= OR_R_SCALING;
         break;
     }
+    case OR_LAYERWISE: {
+        /* "the hybrid strategy could be more complex when applying different parallel
+         * strategies for different layers"; "there can be cases at which a
+         * different type of parallelism is used ... the fully connected layer in spatial
+         * parallelism is not spatially parallelized".  Q39: every COMM row (in row
+         * order, bit j of the mask for the j-th) is data-parallel (0) or filter-parallel (1)
+         * over the same p PEs; other rows follow the COMM row before them (the first COMM
+         * row's strategy before it).  Mini-batch B = b p: a data row holds b samples and
+         * the whole weights (Data row of Table 2), a filter row all B samples
+         * and 1/p of the weights (Filter row).
+         *   comp = ((B FB)/p) tau + (WU_D + WU_F/p) tau
+         *   GE   = AR(p, delta W_D) over the data rows' weights (absent if every COMM row is F)
+         *   AG   = (p-1)(NC_F alpha + (B delta YC_F / p) beta)  (filter rows' Allgathers, Q10)
+         *        + (p-1)(n_T alpha + (b delta Y_T) beta)      (strategy changes, below)
+         *   AR   = 2 x the filter rows' Allgather term (1 x with filter_rs, P:355 fn)
+         *   mem  = gamma (delta (((2B XY_D)/p + 2B XY_F) + (2W_D + (2W_F)/p)) + BI))
+         * A change D -> F at COMM row l gathers the b-sample activations y_{l-1} of every
+         * PE (Allgather, forward) and reduce-scatters dL/dx back (backward); F -> D
+         * gathers the b-sample gradients dL/dy_{l-1} (Allgather, backward): per-PE segment
+         * b |y_{l-1}| each (P:553-556 ring steps), so n_T = 2 n_DF + n_FD and Y_T =
+         * 2 sum_DF y_{l-1} + sum_FD y_{l-1}.  Limit: p <= min F over the filter COMM rows. */
+        p = d[0];
+        if (d[1] != 1 || d[2] != 1 || d[3] != 1) FAIL(E_INVAL, "layerwise dims are (p,1,1,1)");
+        if (!mul_ok(b, p, &B)) FAIL(E_OVERFLOW, "b*p");
+        const uint64_t mask = c->i_part;
+        int64_t FB = 0, WUD = 0, WUF = 0, WD = 0, WF = 0, XYD = 0, XYF = 0, BI = 0;
+        int64_t NCF = 0, YCF = 0, nT = 0, YT = 0, FminF = INT64_MAX, ncomm = 0, nF = 0;
+        int64_t last_comm = -1, first_comm = -1;
+        for (int64_t l = 0; l < m->G; l++)
+            if (m->rows[l].flags & OR_FLAG_COMM) { if (first_comm < 0) first_comm = l; last_comm = l; }
+        int cur = first_comm >= 0 ? (int)(mask & 1) : 0;   /* strategy of the rows: 0 D, 1 F */
+        for (int64_t l = 0; l < m->G; l++) {
+            const or_layer *r = &m->rows[l];
+            if (r->flags & OR_FLAG_COMM) {
+                int sf = (int)((mask >> ncomm) & 1);
+                if (ncomm > 0 && sf != cur) {
+                    const int64_t yb = m->rows[l - 1].y;
+                    nT += sf ? 2 : 1;
+                    YT += sf ? 2 * yb : yb;
+                }
+                cur = sf;
+                ncomm++;
+                if (cur) {
+                    nF++;
+                    if (r->F < FminF) FminF = r->F;
+                    if (l != last_comm) { NCF += 1; YCF += r->y; }
+                }
+            }
+            FB += r->fw + r->bw;
+            BI += r->bi;
+            if (cur) { WUF += r->wu; WF += r->w; XYF += r->x + r->y; }
+            else     { WUD += r->wu; WD += r->w; XYD += r->x + r->y; }
+        }
+        int64_t BFB, tBXYD, tBXYF, BdYCF, bdYT, dWD;
+        if (!mul_ok(B, FB, &BFB) || !mul_ok(2 * B, XYD, &tBXYD) || !mul_ok(2 * B, XYF, &tBXYF) ||
+            !mul_ok(B * delta, YCF, &BdYCF) || !mul_ok(b * delta, YT, &bdYT) || !mul_ok(delta, WD, &dWD))
+            FAIL(E_OVERFLOW, "layerwise sums");
+        comp = ((double)BFB / (double)p) * tau + ((double)WUD + (double)WUF / (double)p) * tau;
+        int t = tier_or_flag(sys, p, &reason);
+        const int all_f = ncomm > 0 && nF == ncomm;
+        if (!all_f)
+            ge = t < 0 ? INFINITY
+                       : t_allreduce(sys, p, (double)dWD, (double)dWD / (double)p, c->alpha[t], c->beta[t]);
+        if (p > 1 && (nF > 0 || nT > 0)) {   /* no filter row and no change: no exchange at all */
+            double agf = t < 0 ? INFINITY
+                               : (double)(p - 1) * ((double)NCF * c->alpha[t] + ((double)BdYCF / (double)p) * c->beta[t]);
+            double tr = t < 0 ? INFINITY
+                              : (double)(p - 1) * ((double)nT * c->alpha[t] + (double)bdYT * c->beta[t]);
+            ag = agf + tr;
+            ar = (sys->filter_rs ? 1.0 : 2.0) * agf;
+        }
+        mem = sys->gamma * ((double)delta * ((((double)tBXYD / (double)p + (double)tBXYF) +
+                                              ((double)(2 * WD) + (double)(2 * WF) / (double)p)) +
+                                             (double)BI));
+        if (nF > 0 && p > FminF) reason |= OR_R_SCALING;
+        break;
+    }
     case OR_SPATIAL_AG: {
         /* "we implement the spatial strategy for some first layers ... We then
          * implement an Allgather to collect the full set of activations before passing
@@ -831,6 +923,41 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
             if (c->n_stages > 1 && ts >= 0) o->t_p2p = 2.0 * sumP2P;
         } else {
             o->t_comp = (double)(c->n_stages + c->S - 1) / (double)c->S * (double)b * (mF + mB) + mU;
+        }
+    }
+    if (fam == OR_LAYERWISE) {
+        /* per-row fold: each row with its own strategy's divisors; Allgather / transition
+         * terms one message at a time */
+        const uint64_t mask = c->i_part;
+        int64_t last_comm = -1, first_comm = -1, ncomm = 0;
+        for (int64_t l = 0; l < m->G; l++)
+            if (m->rows[l].flags & OR_FLAG_COMM) { if (first_comm < 0) first_comm = l; last_comm = l; }
+        int cur = first_comm >= 0 ? (int)(mask & 1) : 0;
+        double comp = 0.0, mem = 0.0, agf = 0.0, tr = 0.0;
+        int t = tier_of(sys, p);
+        const double a = t >= 0 ? c->alpha[t] : 0.0, be = t >= 0 ? c->beta[t] : 0.0;
+        for (int64_t l = 0; l < m->G; l++) {
+            const or_layer *r = &m->rows[l];
+            if (r->flags & OR_FLAG_COMM) {
+                int sf = (int)((mask >> ncomm) & 1);
+                if (ncomm > 0 && sf != cur) {
+                    double one = a + (double)b * (double)m->rows[l - 1].y * dl * be;
+                    tr += sf ? 2.0 * one : one;
+                }
+                cur = sf;
+                ncomm++;
+                if (cur && l != last_comm) agf += a + ((double)B * (double)r->y / (double)p) * dl * be;
+            }
+            comp += ((double)B / (double)p) * ((double)r->fw * tau + (double)r->bw * tau);
+            comp += ((double)r->wu * tau) / (cur ? (double)p : 1.0);
+            mem += dl * ((2.0 * (double)B) * (double)(r->x + r->y) / (cur ? 1.0 : (double)p) +
+                         2.0 * (double)r->w / (cur ? (double)p : 1.0) + (double)r->bi);
+        }
+        o->t_comp = comp;
+        o->mem = sys->gamma * mem;
+        if (p > 1 && t >= 0 && o->t_fb_ag != 0.0) {
+            o->t_fb_ag = (double)(p - 1) * agf + (double)(p - 1) * tr;
+            o->t_fb_ar = (sys->filter_rs ? 1.0 : 2.0) * (double)(p - 1) * agf;
         }
     }
     o->t_iter = ((((o->t_comp + o->t_ge) + o->t_fb_ag) + o->t_fb_ar) + o->t_halo) + o->t_p2p;

@@ -27,6 +27,9 @@ enum { OR_SERIAL = 0, OR_DATA, OR_SPATIAL, OR_FILTER, OR_CHANNEL, OR_DF, OR_DS,
        OR_GPIPE,        /* pipeline timed by the GPipe schedule itself (Q36) */
        OR_DATA_LW,      /* data parallel, one gradient Allreduce per weighted layer, each message
                          * ring or tree by its size (Q37) */
+       OR_LAYERWISE,    /* per-layer strategy: every COMM row data- or filter-parallel over the
+                         * same p PEs, with activation exchanges at strategy changes (P:413,
+                         * P:450; Q39).  MASK partition radix over the COMM rows. */
        OR_N_FAMILIES };
 enum { OR_PART_NONE = 0, OR_PART_COMB = 1, OR_PART_MASK = 2 };
 /* infeasibility reasons (bit set) */

@@ -20,7 +20,11 @@ R_SCALING, R_MEMORY, R_SPLIT, R_TIER, R_SEGMENTS = 1, 2, 4, 8, 16
 
 
 # ------------------------------------------------------------------ enumeration
-def partitions(G, sub):
+def partitions(G, sub, model=None):
+    if sub.family == W.LAYERWISE:
+        # one strategy bit per COMM row (Q39): every assignment, mask value ascending
+        nc = sum(1 for r in model.layers if r.flags & M.FLAG_COMM)
+        return [("lw", mask) for mask in range(1 << nc)]
     if sub.family not in W.PIPE_FAMILIES:
         return [(G,)]
     if sub.part_mode == W.PART_MASK:
@@ -49,7 +53,7 @@ def enumerate_configs(sweep):
         Lss = sub.Ls or [0]
         alphas = sub.alpha or [[t.alpha for t in sys.tiers]]
         betas = sub.beta or [[t.beta for t in sys.tiers]]
-        parts = partitions(m.G, sub)
+        parts = partitions(m.G, sub, m)
         for cap, R, b, part, S, dims, Ls, a, bb in itertools.product(
                 caps, flops, sub.b, parts, Ss, dimss, Lss, alphas, betas):
             yield idx, dict(sub=si, family=sub.family, model=sub.model, cap=cap, R=R, b=b,
@@ -182,6 +186,53 @@ def exact(sweep, cfg):
                                        for r in L if r.w > 0)
         mem = mem_row(B, p, 1)
         if p > B:
+            reason |= R_SCALING
+    elif fam == W.LAYERWISE:
+        # per-layer data / filter strategy over the same p PEs (Q39): every
+        # row is evaluated with its own Table 2 row (Data P:469-473 with b samples, Filter
+        # P:493-498 with all B samples) and the activations cross a strategy change by one
+        # Allgather (D -> F forward, F -> D backward) and one Reduce-Scatter (D -> F
+        # backward) of the b-sample boundary tensor
+        p = p1
+        B = b * p
+        mask = cfg["ends"][1]
+        strat = []
+        cur = None
+        j = 0
+        for r in L:
+            if r.flags & M.FLAG_COMM:
+                cur = (mask >> j) & 1
+                j += 1
+            strat.append(cur)
+        first = next((s_ for s_ in strat if s_ is not None), 0)
+        strat = [first if s_ is None else s_ for s_ in strat]
+        comp = sum(Fr(B, p) * (r.fw + r.bw) * tau for r in L) + sum(Fr(r.wu, p if f else 1) * tau
+                                                                    for r, f in zip(L, strat))
+        t = tier(p)
+        has_d = not comm_rows or any(strat[l] == 0 for l in comm_rows)
+        if has_d:
+            WD = sum(r.w for r, f in zip(L, strat) if not f)
+            ge = inf if t is None else ar_exact(sys, p, Fr(dl * WD), Fr(dl * WD, p), A[t], Bt[t])
+        n_f = sum(1 for l in comm_rows if strat[l])
+        changes = sum(1 for i in range(1, len(comm_rows)) if strat[comm_rows[i]] != strat[comm_rows[i - 1]])
+        if p > 1 and (n_f or changes):
+            if t is None:
+                ag = ar = inf
+            else:
+                msg = [A[t] + Fr(B * L[l].y, p) * dl * Bt[t] for l in Cm if strat[l]]
+                agf = (p - 1) * sum(msg)
+                tr = Fr(0)
+                for i in range(1, len(comm_rows)):
+                    l = comm_rows[i]
+                    if strat[l] != strat[comm_rows[i - 1]]:
+                        one = (p - 1) * (A[t] + b * L[l - 1].y * dl * Bt[t])
+                        tr += 2 * one if strat[l] else one
+                ag = agf + tr
+                ar = (1 if sys.filter_rs else 2) * agf
+        mem = gamma * dl * sum(Fr(2 * B * (r.x + r.y), 1 if f else p) + Fr(2 * r.w, p if f else 1) + r.bi
+                               for r, f in zip(L, strat))
+        lim = min((L[l].F for l in comm_rows if strat[l]), default=None)
+        if lim is not None and p > lim:
             reason |= R_SCALING
     elif fam == W.SPATIAL_AG:
         # spatial on rows [0, Ls), Allgather of y_Ls, rows [Ls, G) replicated (Q35)
@@ -427,6 +478,20 @@ def buffer_bytes(sweep, cfg):
     elif fam in (W.SPATIAL, W.DS):
         p2 = d1 * d2 * d3
         tot = sum(layer_bufs(r, b * p1, p1 * p2, 1) for r in L)     # spatial shard of the group batch
+    elif fam == W.LAYERWISE:
+        # data rows hold b = B/p samples and whole weights, filter rows all B samples and
+        # 1/p of the weights (Q39)
+        B = b * p1
+        mask = cfg["ends"][1]
+        strat, cur, j = [], None, 0
+        for r in L:
+            if r.flags & M.FLAG_COMM:
+                cur = (mask >> j) & 1
+                j += 1
+            strat.append(cur)
+        first = next((s_ for s_ in strat if s_ is not None), 0)
+        strat = [first if s_ is None else s_ for s_ in strat]
+        tot = sum(layer_bufs(r, B, 1, p1) if f else layer_bufs(r, B, p1, 1) for r, f in zip(L, strat))
     elif fam == W.SPATIAL_AG:
         p2 = d1 * d2 * d3
         Lp = min(cfg["Ls"], len(L))

@@ -643,3 +643,30 @@ def test_compact_full_size_windows(dev, oracle_mod, cfg):
     rng = random.Random(300 + cfg)
     for a in [0, n - 5000] + [rng.randrange(n - 5000) for _ in range(6)]:
         check_compact(ctx, spec, osw, a, rng.randrange(1000, 5000), dev)
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_full_sweep_chunks_vs_oracle_golden(dev, cfg):
+    """Whole-sweep oracle runs in progress (tools/golden_full.py checkpoints): every finished
+    chunk of 2^30 consecutive configurations -- its top-64 and feasible count, oracle only --
+    against the GPU's top-64 + count over the same range."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", f"full_cfg{cfg}.chunks.jsonl")
+    if not os.path.exists(p):
+        pytest.skip(f"no chunk goldens for cfg{cfg}")
+    sw = W.CONFIGS[cfg]()
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    n = ctx.sweep_size(spec)
+    done = 0
+    for ln in open(p):
+        r = json.loads(ln)
+        assert r["n"] == n
+        hits, nf = ctx.topk(spec, 64, r["first"], r["count"])
+        assert nf == r["n_feasible"]
+        gh = r["hits"]
+        assert [h[0] for h in hits[:len(gh)]] == [i for i, _ in gh]
+        assert [h[1] for h in hits[:len(gh)]] == [float.fromhex(k) for _, k in gh]
+        done += 1
+    assert done > 0

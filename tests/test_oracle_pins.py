@@ -271,6 +271,100 @@ def test_pd_ge_equals_concurrent_rings(oracle_mod, pd, ws):
     assert pr1.t_ge == 0.0
 
 
+@pytest.mark.parametrize("seed", range(20))
+def test_layerwise_reduces_to_data_and_filter(oracle_mod, seed):
+    """Per-layer strategy (Q39): every COMM row data-parallel is the Data row of
+    Table 2 and every COMM row filter-parallel is the Filter row at
+    mini-batch b p, bit for bit (tolerance 0), for every p including p = 1."""
+    m = corpus.random_model(seed)
+    sysd = corpus.random_system(seed)
+    nt = len(sysd.tiers)
+    A = [[1e-5 * (t + 1) for t in range(nt)], [3e-6 * (t + 2) for t in range(nt)]]
+    Bt = [[1e-9 * (t + 1) for t in range(nt)], [7e-10 * (t + 1) for t in range(nt)]]
+    b = 4
+    P = [1, 2, 3, 4, 8]
+    nc = sum(1 for r in m.layers if r.flags & M.FLAG_COMM)
+    if nc > 10:
+        pytest.skip("too many COMM rows for a full mask enumeration")
+    dims = [(p, 1, 1, 1) for p in P]
+    subs = [W.SubSweep(W.LAYERWISE, b=[b], dims=dims, part_mode=W.PART_MASK, alpha=A, beta=Bt),
+            W.SubSweep(W.DATA, b=[b], dims=dims, alpha=A, beta=Bt)]
+    subs += [W.SubSweep(W.FILTER, b=[b * p], dims=[(p, 1, 1, 1)], alpha=A, beta=Bt) for p in P]
+    sw = W.Sweep([m], sysd, subs, "lw")
+    o = oracle_mod.OracleSweep(sw)
+    fields = ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_halo", "t_p2p", "t_iter", "t_epoch", "mem", "reason", "B", "p")
+    confs = list(brute.enumerate_configs(sw))
+    full = (1 << nc) - 1
+    for idx, cfg in confs:
+        if cfg["sub"] != 0 or cfg["ends"][1] not in (0, full):
+            continue
+        x = o.explain(idx)
+        p = cfg["dims"][0]
+        if cfg["ends"][1] == 0 or nc == 0:
+            want = next(i for i, c in confs if c["sub"] == 1 and c["dims"] == cfg["dims"]
+                        and c["alpha"] == cfg["alpha"] and c["beta"] == cfg["beta"])
+        else:
+            want = next(i for i, c in confs if c["sub"] == 2 + P.index(p)
+                        and c["alpha"] == cfg["alpha"] and c["beta"] == cfg["beta"])
+        y = o.explain(want)
+        for f in fields:
+            assert getattr(x, f) == getattr(y, f), (f, cfg["ends"], p)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_layerwise_matches_exact_rationals(oracle_mod, seed):
+    """Every configuration of the random corpora's per-layer-strategy sub-sweep (Q39) against
+    the exact per-row rational evaluator and the buffer enumeration."""
+    sw = corpus.random_sweep(seed)
+    if sw.subs[-1].family != W.LAYERWISE:
+        pytest.skip("no layerwise sub-sweep in this corpus")
+    o = oracle_mod.OracleSweep(sw)
+    si = len(sw.subs) - 1
+    confs = [(i, c) for i, c in brute.enumerate_configs(sw) if c["sub"] == si]
+    rng = random.Random(seed)
+    for idx, cfg in rng.sample(confs, min(400, len(confs))):
+        pr = o.explain(idx)
+        ex = brute.exact(sw, cfg)
+        assert pr.reason == ex["reason"], (idx, cfg)
+        for f in ("t_comp", "t_ge", "t_fb_ag", "t_fb_ar", "t_iter", "mem", "I"):
+            v = ex[f]
+            got = getattr(pr, f)
+            if v is None:
+                assert math.isinf(got), (f, idx)
+            else:
+                assert _rel(got, v) <= 1e-14, (f, idx, got, float(v))
+        assert _rel(pr.mem, brute.buffer_bytes(sw, cfg)) <= 1e-15
+
+
+def test_layerwise_transitions_are_ring_collectives(oracle_mod):
+    """Strategy changes (Q39): conv rows data-parallel, the FC rows filter-parallel (the
+    'one weird trick' split P:413 cites), so one D -> F change at the first FC row: its
+    input y (b samples per PE) is all-gathered forward and reduce-scattered backward,
+    each the explicit ring simulation; the F rows' own Allgathers follow the
+    Filter row.  Checked against the simulators, not the formula."""
+    a, be = 2e-6, 1.0 / 9e9
+    rows = [toys.row(y=1000, w=50, F=64), toys.row(y=600, w=70, F=64),
+            toys.row(kind=M.FC, y=40, w=900, F=40), toys.row(kind=M.FC, y=10, w=400, F=10)]
+    m = toys.model(rows)
+    p, b = 4, 3
+    sub = W.SubSweep(W.LAYERWISE, b=[b], dims=[(p, 1, 1, 1)], part_mode=W.PART_MASK)
+    sw = toys.sweep(m, toys.system(alpha=a, beta=be, delta=4), [sub])
+    o = oracle_mod.OracleSweep(sw)
+    mask = 0b1100                      # rows 2, 3 filter-parallel
+    pr = o.explain(mask)
+    seg = Fr(b * 600 * 4)              # y_1 of b samples, delta = 4
+    ag_in = brute.ring_allgather_sim(p, seg, Fr(a), Fr(be))
+    full, _ = brute.ring_allreduce_sim(p, seg * p, Fr(a), Fr(be))
+    rs_back = full - ag_in             # the ring's reduce-scatter half
+    ag_fc = brute.ring_allgather_sim(p, Fr(b * p * 40 * 4, p), Fr(a), Fr(be))   # row 2 (not the last COMM row)
+    assert _rel(pr.t_fb_ag, ag_fc + ag_in + rs_back) <= 2e-16
+    assert _rel(pr.t_fb_ar, 2 * ag_fc) <= 2e-16
+    back = o.explain(0b0011)           # F -> D at row 2: dL/dy_1 all-gathered backward only
+    ag_fc2 = brute.ring_allgather_sim(p, Fr(b * p * 1000 * 4, p), Fr(a), Fr(be)) + \
+        brute.ring_allgather_sim(p, Fr(b * p * 600 * 4, p), Fr(a), Fr(be))
+    assert _rel(back.t_fb_ag, ag_fc2 + ag_in) <= 4e-16
+
+
 def test_partition_balanced_example(oracle_mod):
     e = EX["partition_balanced"]
     m = toys.model([toys.row(fw=c, bw=0) for c in e["costs"]], D=1)
@@ -568,7 +662,10 @@ def test_decoder_matches_itertools_enumeration(oracle_mod, seed):
         c = o.decode(idx)
         assert c.sub == cfg["sub"] and c.b == cfg["b"] and c.S == cfg["S"]
         assert tuple(c.dims) == tuple(cfg["dims"]) and c.Ls == cfg["Ls"]
-        assert tuple(c.stage_end[:c.n_stages]) == cfg["ends"]
+        if cfg["family"] == W.LAYERWISE:
+            assert c.i_part == cfg["ends"][1] and c.n_stages == 1
+        else:
+            assert tuple(c.stage_end[:c.n_stages]) == cfg["ends"]
         nt = len(sw.system.tiers)
         assert list(c.alpha[:nt]) == list(cfg["alpha"]) and list(c.beta[:nt]) == list(cfg["beta"])
         assert c.cap == cfg["cap"] and c.flops == cfg["R"]

@@ -114,4 +114,14 @@ def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:
                 kw["s_min"] = smin
                 kw["s_max"] = rng.randint(smin, min(m.G, smin + 3, smax_fam))
         subs.append(W.SubSweep(fam, **kw))
+    # per-layer strategy (appended last, so the other sub-sweeps keep their seeds): on the
+    # model with fewer COMM rows, when it has at most 7 (<= 128 assignments)
+    nc = [sum(1 for r in m.layers if r.flags & M.FLAG_COMM) for m in models]
+    mi = 0 if nc[0] <= nc[1] else 1
+    if nc[mi] <= 7:
+        A, B = ab()
+        subs.append(W.SubSweep(W.LAYERWISE, model=mi, part_mode=W.PART_MASK, alpha=A, beta=B,
+                               b=some([1, 2, 3, 8, 32]),
+                               cap=some([2.0 ** 18, 2.0 ** 24, 2.0 ** 30]) if rng.random() < 0.5 else [],
+                               dims=[(p, 1, 1, 1) for p in some([1, 2, 3, 4, 16, 1024])]))
     return W.Sweep(models, sys, subs, f"rand{seed}")

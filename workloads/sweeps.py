@@ -20,8 +20,10 @@ SERIAL, DATA, SPATIAL, FILTER, CHANNEL, DF, DS, PIPELINE, LAYERPURE, PD = range(
 SPATIAL_AG, GPIPE = 10, 11
 # per-layer gradient messages with per-message ring / tree dispatch
 DATA_LW = 12
+# per-layer heterogeneous strategy, one data / filter bit per COMM row
+LAYERWISE = 13
 FAMILY_NAMES = ["serial", "data", "spatial", "filter", "channel", "df", "ds",
-                "pipeline", "layerpure", "pd", "spatial_ag", "gpipe", "data_lw"]
+                "pipeline", "layerpure", "pd", "spatial_ag", "gpipe", "data_lw", "layerwise"]
 PIPE_FAMILIES = (PIPELINE, LAYERPURE, PD, GPIPE)
 SPATIAL_FAMILIES = (SPATIAL, DS, SPATIAL_AG)
 
@@ -239,4 +241,20 @@ def next_data_lw(n_alpha=256, n_beta=256) -> Sweep:
     return Sweep(ms, sys, subs, "next_data_lw")
 
 
-NEXT = {"gpipe": next_gpipe, "spatial_ag": next_spatial_ag, "data_lw": next_data_lw}
+def next_layerwise(n_alpha=32, n_beta=32) -> Sweep:
+    """Per-layer heterogeneous strategy (family LAYERWISE, Q39): every
+    one of VGG16's 16 weighted layers data- or filter-parallel (2^16 assignments, the paper's
+    "fully connected layer ... not spatially parallelized" generalised), p in 2^0..2^10, b in
+    {8, 32, 128}, a 32 x 32 alpha/beta grid; and the CosmoFlow-like 128^3 net's 8 weighted
+    layers (2^8 assignments) with capacities."""
+    vgg, cf = M.vgg16(), M.cosmoflow(128)
+    sys = two_tier_system(flops_per_s=37e12, hbm_bytes=16 * GiB)
+    A, B = ab_grid(np.logspace(-7, -4, n_alpha), 1.0 / np.logspace(9, 12, n_beta))
+    ps = [(p, 1, 1, 1) for p in pow2(0, 10)]
+    subs = [SubSweep(LAYERWISE, model=0, part_mode=PART_MASK, dims=ps, b=[8, 32, 128], alpha=A, beta=B),
+            SubSweep(LAYERWISE, model=1, part_mode=PART_MASK, dims=ps, b=[1, 2, 4],
+                     cap=[16 * GiB, 80 * GiB, 180 * GiB], alpha=A, beta=B)]
+    return Sweep([vgg, cf], sys, subs, "next_layerwise_vgg16_cosmoflow")
+
+
+NEXT = {"gpipe": next_gpipe, "spatial_ag": next_spatial_ag, "data_lw": next_data_lw, "layerwise": next_layerwise}
