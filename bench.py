@@ -46,7 +46,10 @@ M_SLOTS = 2.0
 FP64_OPS_PER_CONFIG = {"pipeline": 4.0, "data": 4.0, "filter": 6.0 + 1 / M_SLOTS, "channel": 6.0 + 1 / M_SLOTS,
                        "spatial": 7.0 + 1 / M_SLOTS, "df": 9.0 + 1 / M_SLOTS, "ds": 10.0 + 1 / M_SLOTS,
                        "pd": 7.0, "layerpure": 4.0 + 1 / M_SLOTS, "serial": 1.0,
-                       "spatial_ag": 10.0 + 1 / M_SLOTS}
+                       "spatial_ag": 10.0 + 1 / M_SLOTS,
+                       # per-layer strategy (Q39): per alpha row 2 (n alpha products), per
+                       # configuration GE 3, Allgather 2, changes 2, ag 1, t folds 2, AR 1, key 1
+                       "layerwise": 14.0}
 
 
 def fp64_per_config(sb) -> float:
@@ -678,6 +681,10 @@ def next_rows(ctx, P, W, stream, flush, my_hits, my_cnt, fp64_peak):
             ctx.prepare(sw)
             opc = ops / max(1, n_feas)
             kern = "sweep_kernel<DATA_LW,reduce>"
+        elif name == "layerwise":
+            opc = FP64_OPS_PER_CONFIG["layerwise"]
+            ops = opc * n_feas
+            kern = "sweep_kernel<LAYERWISE,reduce>"
         else:
             opc = FP64_OPS_PER_CONFIG["spatial_ag"]   # GE 3 + Allgather 3 + halo 3 + 1/M + key 1
             ops = opc * n_feas

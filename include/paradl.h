@@ -70,10 +70,16 @@ enum { PARADL_FLAG_COMM = 1u, PARADL_FLAG_FOLDED = 4u };
  * DATA_LW: dims (p,1,1,1); the Data row with the gradient exchanged as one Allreduce per
  *   weighted layer (message delta |w_l|, row order), each message ring or tree by its size
  *   against tree_threshold_B ("ring ... for large message sizes and a tree-based algorithm
- *   for small message sizes"; tree time P:559; Q37). */
+ *   for small message sizes"; tree time P:559; Q37).
+ * LAYERWISE: dims (p,1,1,1), partition mode MASK with one bit per COMM row (row order):
+ *   1 = that weighted layer is filter-parallel, 0 = data-parallel, over the same p PEs
+ *   ("applying different parallel strategies for different layers"); rows
+ *   between COMM rows follow the COMM row before them.  Mini-batch B = b p.  Strategy
+ *   changes exchange the b-sample boundary activation (Q39).  At most 62 COMM
+ *   rows. */
 enum { PARADL_SERIAL = 0, PARADL_DATA, PARADL_SPATIAL, PARADL_FILTER, PARADL_CHANNEL,
        PARADL_DF, PARADL_DS, PARADL_PIPELINE, PARADL_LAYERPURE, PARADL_PD,
-       PARADL_SPATIAL_AG, PARADL_GPIPE, PARADL_DATA_LW, PARADL_N_FAMILIES };
+       PARADL_SPATIAL_AG, PARADL_GPIPE, PARADL_DATA_LW, PARADL_LAYERWISE, PARADL_N_FAMILIES };
 #define PARADL_GPIPE_MAX_STAGES 8
 
 /* Partition radix of the pipeline families (groups g_i, P:519 footnote).

@@ -24,7 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 A.declare(_lib)
 
 # family / partition constants (same values as include/paradl.h)
-SERIAL, DATA, SPATIAL, FILTER, CHANNEL, DF, DS, PIPELINE, LAYERPURE, PD, SPATIAL_AG, GPIPE, DATA_LW = range(13)
+SERIAL, DATA, SPATIAL, FILTER, CHANNEL, DF, DS, PIPELINE, LAYERPURE, PD, SPATIAL_AG, GPIPE, DATA_LW, LAYERWISE = range(14)
 PART_NONE, PART_COMB, PART_MASK = 0, 1, 2
 
 

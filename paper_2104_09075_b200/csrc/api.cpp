@@ -403,6 +403,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
             case PARADL_SERIAL: case PARADL_PIPELINE: case PARADL_LAYERPURE: case PARADL_GPIPE:
                 ok = d[0] == 1 && d[1] == 1 && d[2] == 1 && d[3] == 1; break;
             case PARADL_DATA: case PARADL_FILTER: case PARADL_CHANNEL: case PARADL_PD: case PARADL_DATA_LW:
+            case PARADL_LAYERWISE:
                 ok = d[1] == 1 && d[2] == 1 && d[3] == 1; break;
             case PARADL_DF: ok = d[2] == 1 && d[3] == 1; break;
             case PARADL_SPATIAL: case PARADL_SPATIAL_AG: ok = d[0] == 1; break;
@@ -410,7 +411,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
             }
             if (!ok) return fail(c, PARADL_EINVAL, "sub %d: dims tuple does not fit the family", i);
             const int64_t deg = (fam == PARADL_DATA || fam == PARADL_DF || fam == PARADL_DS || fam == PARADL_PD ||
-                                 fam == PARADL_DATA_LW)
+                                 fam == PARADL_DATA_LW || fam == PARADL_LAYERWISE)
                                     ? d[0]
                                     : 1;
             degmax = std::max(degmax, deg);
@@ -433,7 +434,14 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         h.part_mode = s.part_mode;
         h.s_min = h.s_max = 1;
         std::vector<uint64_t> sblk, binom;
-        if (!pipe) {
+        if (fam == PARADL_LAYERWISE) {
+            // one strategy bit per COMM row (Q39)
+            if (s.part_mode != PARADL_PART_MASK) return fail(c, PARADL_EINVAL, "sub %d: layerwise needs the mask partition mode", i);
+            int nc = 0;
+            for (const auto &r : m.rows) nc += (r.flags & PARADL_FLAG_COMM) != 0;
+            if (nc > 62) return fail(c, PARADL_EINVAL, "sub %d: layerwise needs at most 62 COMM rows", i);
+            part_n = (uint64_t)1 << nc;
+        } else if (!pipe) {
             if (s.part_mode != PARADL_PART_NONE) return fail(c, PARADL_EINVAL, "sub %d: partition mode on a non-pipeline family", i);
         } else if (s.part_mode == PARADL_PART_MASK) {
             if (G > 64) return fail(c, PARADL_EINVAL, "sub %d: mask mode needs G <= 64", i);
@@ -471,7 +479,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
             const __int128 hv = 6 * m.Hmax * m.XY;
             const __int128 terms[] = {B * m.FB, 2 * B * m.XY, B * dl_ * m.Ysum, (__int128)bmax * dl_ * hv,
                                       dl_ * m.W, 2 * (__int128)bmax * m.XY + 2 * m.W + m.BI,
-                                      dl_ * (__int128)bmax * m.Ysum, (__int128)m.D};
+                                      2 * dl_ * (__int128)bmax * m.Ysum, (__int128)m.D};
             for (__int128 t : terms)
                 if (t < 0 || t >= kLimit) return fail(c, PARADL_EOVERFLOW, "sub %d: an int64 intermediate may exceed 2^62", i);
             if (pmax > ((int64_t)1 << 40)) return fail(c, PARADL_EOVERFLOW, "sub %d: PE count too large", i);

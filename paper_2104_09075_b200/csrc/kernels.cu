@@ -378,10 +378,16 @@ struct Mid {
     double I_memo;
     int64_t bS_b, bS_S;
     double bS_memo;
+    // LAYERWISE: the strategy assignment's row sums, kept while the mask repeats (the dims,
+    // b and slower digits change the products only)
+    uint64_t lw_mask;
+    int64_t lw_WUF, lw_WF, lw_XYF, lw_NCF, lw_YCF, lw_nT, lw_YT, lw_FminF;
+    int32_t lw_ncomm, lw_nF;
     __device__ void reset_memo() {
         R_memo = -1.0;
         B_memo = -1;
         bS_b = bS_S = -1;
+        lw_mask = ~0ull;
     }
 };
 
@@ -578,6 +584,85 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.gns = ns;
         m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
         if (Sg > b) reason |= PARADL_R_SEGMENTS;
+    } else if (FAM == PARADL_LAYERWISE) {
+        // Per-layer strategy (Q39): bit j of the partition digit
+        // makes the j-th COMM row filter-parallel (else data-parallel) over the same p PEs;
+        // other rows follow the COMM row before them.  Exact int64 sums over the rows by
+        // prefix differences: WU, W, XY of the data (D) and filter (F) rows, the filter COMM
+        // rows' Allgather messages (NC_F, YC_F; the model's last COMM row excluded, Q10) and
+        // limit (min F), the strategy changes (n_T messages of Y_T b-sample elements).
+        p = dm[0];
+        B = b * p;
+        const RowGeo *geo = at<RowGeo>(v.mb, M->off_geo);
+        const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+        const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+        const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+        const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+        const uint64_t mask = L.part;
+        const int G = M->G;
+        if (mask != m.lw_mask) {
+            m.lw_mask = mask;
+            int last_comm = -1, first_comm = -1;
+            for (int l = 0; l < G; l++)
+                if (geo[l].flags & PARADL_FLAG_COMM) {
+                    if (first_comm < 0) first_comm = l;
+                    last_comm = l;
+                }
+            int cur = first_comm >= 0 ? (int)(mask & 1) : 0;
+            int64_t WUF = 0, WF = 0, XYF = 0, NCF = 0, YCF = 0, nT = 0, YT = 0, FminF = INT64_MAX;
+            int ncomm = 0, nF = 0;
+            for (int l = 0; l < G; l++) {
+                if (geo[l].flags & PARADL_FLAG_COMM) {
+                    const int sf = (int)((mask >> ncomm) & 1);
+                    if (ncomm > 0 && sf != cur) {
+                        nT += sf ? 2 : 1;
+                        YT += sf ? 2 * Y[l - 1] : Y[l - 1];
+                    }
+                    cur = sf;
+                    ncomm++;
+                    if (cur) {
+                        nF++;
+                        FminF = min(FminF, (int64_t)geo[l].F);
+                        if (l != last_comm) {
+                            NCF++;
+                            YCF += Y[l];
+                        }
+                    }
+                }
+                if (cur) {
+                    WUF += PU[l + 1] - PU[l];
+                    WF += PW[l + 1] - PW[l];
+                    XYF += PX[l + 1] - PX[l];
+                }
+            }
+            m.lw_WUF = WUF, m.lw_WF = WF, m.lw_XYF = XYF, m.lw_NCF = NCF, m.lw_YCF = YCF;
+            m.lw_nT = nT, m.lw_YT = YT, m.lw_FminF = FminF, m.lw_ncomm = ncomm, m.lw_nF = nF;
+        }
+        const int64_t WUF = m.lw_WUF, WF = m.lw_WF, XYF = m.lw_XYF, NCF = m.lw_NCF, YCF = m.lw_YCF;
+        const int64_t nT = m.lw_nT, YT = m.lw_YT, FminF = m.lw_FminF;
+        const int ncomm = m.lw_ncomm, nF = m.lw_nF;
+        const int64_t WUD = M->WU - WUF, WD = M->W - WF, XYD = M->XY - XYF;
+        // comp = ((B FB)/p) tau + (WU_D + WU_F/p) tau
+        m.comp = dadd(dmul(div_i(B * M->FB, p), tau), dmul(dadd(i2d(WUD), div_i(WUF, p)), tau));
+        const int t = tier_of(H, p);
+        reason |= flag_tier(t);
+        m.ge.c = m.ge.s = 0.0;   // no data row (every COMM row filter-parallel): no gradient Allreduce
+        m.ge.t = t;
+        if (!(ncomm > 0 && nF == ncomm)) m.ge = make_ar(H, p, i2d(delta * WD), div_i(delta * WD, p), t);
+        m.ag_on = p > 1 && (nF > 0 || nT > 0);
+        m.ag_c = i2d(p - 1);
+        m.ag_na = i2d(NCF);
+        m.ag_s = div_i(B * delta * YCF, p);
+        m.ag_t = t;
+        m.pp_on = m.ag_on;   // strategy changes: (p - 1)(n_T alpha + (b delta Y_T) beta)
+        m.pp_c = m.ag_c;
+        m.pp_na = i2d(nT);
+        m.pp_s = i2d(b * delta * YT);
+        m.pp_t = t;
+        m.mem = dmul(H->gamma, dmul(i2d(delta), dadd(dadd(dadd(div_i(2 * B * XYD, p), i2d(2 * B * XYF)),
+                                                          dadd(i2d(2 * WD), div_i(2 * WF, p))),
+                                                     i2d(M->BI))));
+        if (nF > 0 && p > FminF) reason |= PARADL_R_SCALING;
     } else if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL) {   // Filter / Channel rows
         p = dm[0];
         B = b;
@@ -899,6 +984,21 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
             t = dadd(dadd(t, ag), ar);
         }
     }
+    if (FAM == PARADL_LAYERWISE) {
+        ge = ar_eval(m.ge, 1.0, false);
+        if (m.ge.on) t = dadd(t, ge);
+        if (m.ag_on) {
+            double agf, tr;
+            if (EXPLAIN && m.ag_t < 0) agf = tr = CUDART_INF;
+            else {
+                agf = dmul(m.ag_c, dadd(dmul(m.ag_na, arow[m.ag_t]), dmul(m.ag_s, brow[m.ag_t])));
+                tr = dmul(m.pp_c, dadd(dmul(m.pp_na, arow[m.pp_t]), dmul(m.pp_s, brow[m.pp_t])));
+            }
+            ag = dadd(agf, tr);
+            ar = dmul(m.ar_mult, agf);
+            t = dadd(dadd(t, ag), ar);
+        }
+    }
     if (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG) {
         if (m.h_on) {
             if (EXPLAIN && m.h_t < 0) halo = CUDART_INF;
@@ -962,8 +1062,12 @@ struct SlotV {
 template <int FAM>
 __device__ __forceinline__ void alpha_vals(const Mid &m, const double *arow, AlphaV &a) {
     if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_DF ||
-        FAM == PARADL_SPATIAL_AG)
+        FAM == PARADL_SPATIAL_AG || FAM == PARADL_LAYERWISE)
         a.ge = arow[m.ge.t];
+    if (FAM == PARADL_LAYERWISE) {
+        a.ag = dmul(m.ag_na, arow[m.ag_t]);
+        a.pp = dmul(m.pp_na, arow[m.pp_t]);
+    }
     if (FAM == PARADL_DS) a.ge2 = arow[m.ge2.t];
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) a.ag = dmul(m.ag_na, arow[m.ag_t]);
     if (FAM == PARADL_SPATIAL_AG) a.ag = arow[m.ag_t];
@@ -974,8 +1078,13 @@ __device__ __forceinline__ void alpha_vals(const Mid &m, const double *arow, Alp
 
 template <int FAM>
 __device__ __forceinline__ void slot_vals(const Mid &m, const double *brow, SlotV &v) {
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG)
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG ||
+        FAM == PARADL_LAYERWISE)
         v.ge = dmul(m.ge.s, brow[m.ge.t]);
+    if (FAM == PARADL_LAYERWISE) {
+        v.ag = dmul(m.ag_s, brow[m.ag_t]);
+        v.pp = dmul(m.pp_s, brow[m.pp_t]);
+    }
     if (FAM == PARADL_DF) v.ge = dmul(m.ge.s, dmul(brow[m.ge.t], m.phi));
     if (FAM == PARADL_DS) v.ge2 = dmul(m.ge2.s, brow[m.ge2.t]);
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF || FAM == PARADL_SPATIAL_AG)
@@ -990,6 +1099,11 @@ __device__ __forceinline__ double combine(const Mid &m, const AlphaV &a, const S
     if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DF || FAM == PARADL_SPATIAL_AG)
         t = dadd(t, dmul(m.ge.c, dadd(a.ge, v.ge)));
     if (FAM == PARADL_SPATIAL_AG) t = dadd(t, dmul(m.ag_c, dadd(a.ag, v.ag)));
+    if (FAM == PARADL_LAYERWISE) {
+        t = dadd(t, dmul(m.ge.c, dadd(a.ge, v.ge)));
+        const double agf = dmul(m.ag_c, dadd(a.ag, v.ag));
+        t = dadd(dadd(t, dadd(agf, dmul(m.pp_c, dadd(a.pp, v.pp)))), dmul(m.ar_mult, agf));
+    }
     if (FAM == PARADL_DS) t = dadd(t, dadd(dmul(m.ge.c, dadd(a.ge, v.ge)), dmul(m.ge2.c, dadd(a.ge2, v.ge2))));
     if (FAM == PARADL_FILTER || FAM == PARADL_CHANNEL || FAM == PARADL_DF) {
         const double ag = dmul(m.ag_c, dadd(a.ag, v.ag));
@@ -1242,7 +1356,7 @@ __device__ __forceinline__ void run_slots(const Mid &m, WarpTopK &tk, const doub
     constexpr int KEYS = FAM == PARADL_PIPELINE                                ? PARADL_PIPE_KEYS
                          : (FAM == PARADL_DATA || FAM == PARADL_LAYERPURE) ? 16
                          : (FAM == PARADL_SPATIAL || FAM == PARADL_DS || FAM == PARADL_DF ||
-                            FAM == PARADL_SPATIAL_AG)                                             ? 4
+                            FAM == PARADL_SPATIAL_AG || FAM == PARADL_LAYERWISE)                  ? 4
                                                                                                   : 8;
     constexpr int R = KEYS / M;
     const double *ap = alpha_tab + (size_t)a * NT;
@@ -3156,6 +3270,7 @@ __global__ void explain_kernel(const uint8_t *img, int32_t sub, uint64_t local, 
     Lane L;
     decode(v, local, L, cuts, 1);
     const SubHdr *S = v.S;
+    if (S->family == PARADL_LAYERWISE) L.ns = 1;   // the mask is a strategy assignment, not stages
     cfg->sub = sub;
     cfg->family = S->family;
     cfg->model_id = S->model;
@@ -3208,6 +3323,7 @@ __global__ void explain_kernel(const uint8_t *img, int32_t sub, uint64_t local, 
     case PARADL_SPATIAL_AG: explain_one<PARADL_SPATIAL_AG>(v, L, cuts, cfg, pr); break;
     case PARADL_GPIPE: explain_one<PARADL_GPIPE>(v, L, cuts, cfg, pr); break;
     case PARADL_DATA_LW: explain_one<PARADL_DATA_LW>(v, L, cuts, cfg, pr); break;
+    case PARADL_LAYERWISE: explain_one<PARADL_LAYERWISE>(v, L, cuts, cfg, pr); break;
     default: break;
     }
 }
@@ -3526,6 +3642,7 @@ static void *sweep_fn(int family, bool dense, int blk) {
         PARADL_CASE(PARADL_SPATIAL_AG)
         PARADL_CASE(PARADL_GPIPE)
         PARADL_CASE(PARADL_DATA_LW)
+        PARADL_CASE(PARADL_LAYERWISE)
     default: return nullptr;
     }
 #undef PARADL_CASE

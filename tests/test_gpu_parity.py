@@ -393,7 +393,9 @@ def test_merge_records_equals_single(dev):
                                      ("gpipe", dict(n_alpha=2, n_beta=32, b_list=[8], s_max=2, S_list=(1, 3, 8))),
                                      ("spatial_ag", dict(n_alpha=3, n_beta=2)),
                                      ("data_lw", dict(n_alpha=3, n_beta=5)),
-                                     ("data_lw", dict(n_alpha=2, n_beta=64))])
+                                     ("data_lw", dict(n_alpha=2, n_beta=64)),
+                                     ("layerwise", dict(n_alpha=3, n_beta=2)),
+                                     ("layerwise", dict(n_alpha=2, n_beta=32))])
 def test_next_rows_reduced(dev, oracle_mod, name, kw):
     """GPipe schedule family and spatial prefix + Allgather family on reduced sweeps: whole
     range dense + top-64 against the oracle, then random windows (ragged tails)."""
@@ -414,7 +416,7 @@ def test_next_rows_reduced(dev, oracle_mod, name, kw):
         check_topk(ctx, spec, osw, a, c, 16)
 
 
-@pytest.mark.parametrize("name", ["gpipe", "spatial_ag", "data_lw"])
+@pytest.mark.parametrize("name", ["gpipe", "spatial_ag", "data_lw", "layerwise"])
 def test_next_rows_full_size(dev, oracle_mod, name):
     """Full-size next-row sweeps (the bench's launch configuration): dense windows and
     window top-k against the oracle; whole-sweep top-k hits re-evaluated one by one."""
