@@ -139,6 +139,14 @@ typedef struct {
     int32_t tree_chunks;        /* k >= 1 of the tree form */
     int32_t filter_rs;          /* 0: filter/channel/df backward dL/dx exchange is an Allreduce (Table 2);
                                    1: a Reduce-Scatter, (p-1)(alpha + (m/p) beta) (P:355 footnote; Q38) */
+    /* Point-to-point patterns (spatial / ds halo exchange, pipeline / layer-pure / GPipe
+     * boundary sends) use alpha x p2p_alpha_scale and beta x p2p_beta_scale of their tier,
+     * collectives the tier itself ("different network parameters ... for MPI and NCCL",
+     * P:768-769; Q40).  > 0; 1 = Table 2 literal. */
+    double p2p_alpha_scale, p2p_beta_scale;
+    /* >= 1: contention on the pd stage Allreduces when s > 1 run at once, and on the ds
+     * reduce-to-leader when p1 > 1 groups reduce at once (beta x phi; Q40). */
+    double phi_pd, phi_ds;
 } paradl_system;
 
 /* Base system: default alpha/beta per tier, R, capacity (sweeps may override per radix). */

@@ -244,6 +244,12 @@ static int tier_of(const or_system *sys, int64_t span)
     return -1;
 }
 
+/* Point-to-point parameters of tier t (Q40): the collective tier's alpha and beta times the
+ * system's p2p scales ("we plugged different network parameters in ParaDL ... for MPI and
+ * NCCL"). */
+static double p2p_alpha(const or_system *sys, const or_config *c, int t) { return c->alpha[t] * sys->p2p_alpha_scale; }
+static double p2p_beta(const or_system *sys, const or_config *c, int t) { return c->beta[t] * sys->p2p_beta_scale; }
+
 /* Allreduce over n PEs of an m-byte buffer (P:556 ring: 2(p-1)(alpha + (m/p) beta);
  * P:559 footnote tree: 2(log p + k)(alpha + m/(2k) beta), Q18).  `seg` is the ring
  * step segment the caller's Table 2 row prints (m/p for data, sum|w|/p for df). */
@@ -457,14 +463,17 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         /* FB-Halo per iteration: 2 sum_{l in Sp}(2 alpha + b delta beta (halo(x_l)+halo(dy_l))) */
         if (p2 > 1)
             halo = ti < 0 ? INFINITY
-                          : 2.0 * ((double)(2 * NS) * c->alpha[ti] + (double)bdHV * c->beta[ti]);
+                          : 2.0 * ((double)(2 * NS) * p2p_alpha(sys, c, ti) + (double)bdHV * p2p_beta(sys, c, ti));
         if (c->family == OR_SPATIAL) {
             ge = to < 0 ? INFINITY
                         : t_allreduce(sys, p, (double)dW, (double)dW / (double)p, c->alpha[to], c->beta[to]);
         } else {
-            /* reduce to a leader inside the group, then Allreduce between leaders */
+            /* reduce to a leader inside the group, then Allreduce between leaders;
+             * the p1 groups reduce at once: contention phi_ds when p1 > 1 (Q40) */
+            const double phi = p1 > 1 ? sys->phi_ds : 1.0;
             double rl = ti < 0 ? INFINITY
-                               : t_allreduce(sys, p2, (double)dW, (double)dW / (double)p2, c->alpha[ti], c->beta[ti]);
+                               : t_allreduce(sys, p2, (double)dW, (double)dW / (double)p2, c->alpha[ti],
+                                             c->beta[ti] * phi);
             double al = to < 0 ? INFINITY
                                : t_allreduce(sys, p1, (double)dW, (double)dW / (double)p1, c->alpha[to], c->beta[to]);
             ge = rl + al;
@@ -536,7 +545,8 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
             if (!mul_ok(delta * b, st.sumY, &dBY)) FAIL(E_OVERFLOW, "delta*B*y");
             /* 2 sum_{i<p} T_p2p(delta B |y_{G_i}|) */
             if (ns > 1)
-                p2p = ts < 0 ? INFINITY : 2.0 * ((double)(ns - 1) * c->alpha[ts] + (double)dBY * c->beta[ts]);
+                p2p = ts < 0 ? INFINITY
+                             : 2.0 * ((double)(ns - 1) * p2p_alpha(sys, c, ts) + (double)dBY * p2p_beta(sys, c, ts));
         } else {
             /* (p+S-1)(B/S)(max FW + max BW) + max WU  (per iteration, Q4/Q7) */
             double cseg = (double)(ns + S - 1) * ((double)b / (double)S);
@@ -545,12 +555,15 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
             if (ns > 1)
                 p2p = ts < 0 ? INFINITY
                              : (double)(2 * (ns + S - 2)) *
-                                   (c->alpha[ts] + (((double)b / (double)S) * (double)(delta * st.maxY)) * c->beta[ts]);
+                                   (p2p_alpha(sys, c, ts) +
+                                    (((double)b / (double)S) * (double)(delta * st.maxY)) * p2p_beta(sys, c, ts));
             if (c->family == OR_PD) {
                 int tp = tier_or_flag(sys, p, &reason);
                 double mW = (double)(delta * st.maxW);
+                /* the s stage Allreduces run at once: contention phi_pd when s > 1 (Q40) */
+                const double phi = ns > 1 ? sys->phi_pd : 1.0;
                 if (tp < 0) ge = pd > 1 ? INFINITY : 0.0;
-                else ge = t_allreduce(sys, pd, mW, mW / (double)pd, c->alpha[tp], c->beta[tp]);
+                else ge = t_allreduce(sys, pd, mW, mW / (double)pd, c->alpha[tp], c->beta[tp] * phi);
             }
         }
         mem = sys->gamma * ((double)delta * (double)st.memI);
@@ -691,7 +704,7 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
         if (!mul_ok(b * delta, HV, &bdHV)) FAIL(E_OVERFLOW, "b*delta*HV");
         int t = tier_or_flag(sys, p, &reason);
         if (p > 1)
-            halo = t < 0 ? INFINITY : 2.0 * ((double)(2 * NS) * c->alpha[t] + (double)bdHV * c->beta[t]);
+            halo = t < 0 ? INFINITY : 2.0 * ((double)(2 * NS) * p2p_alpha(sys, c, t) + (double)bdHV * p2p_beta(sys, c, t));
         ge = t < 0 ? INFINITY : t_allreduce(sys, p, (double)dW, (double)dW / (double)p, c->alpha[t], c->beta[t]);
         /* Allgather of y_Ls after the prefix: (p-1)(alpha + (B delta |y_Ls| / p) beta) */
         if (Lp < m->G && p > 1)
@@ -741,7 +754,7 @@ int or_eval(const or_model *models, const or_system *sys, const or_config *c, or
                 uq[i] = (double)U * tau;
                 cq[i] = 0.0;
                 if (i < ns - 1)
-                    cq[i] = c->alpha[ts] + (mb * (double)(delta * m->rows[c->stage_end[i] - 1].y)) * c->beta[ts];
+                    cq[i] = p2p_alpha(sys, c, ts) + (mb * (double)(delta * m->rows[c->stage_end[i] - 1].y)) * p2p_beta(sys, c, ts);
                 beg = c->stage_end[i];
             }
             /* forward wave: segment j enters stage i when stage i is free and stage i-1
@@ -844,7 +857,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
                 const or_layer *r = &m->rows[l];
                 if (r->kind != OR_CONV && r->kind != OR_POOL) continue;
                 double hv = (double)(or_halo_elements(r, split, 0) + or_halo_elements(r, split, 1));
-                sum += 2.0 * c->alpha[t] + (double)b * dl * c->beta[t] * hv;
+                sum += 2.0 * p2p_alpha(sys, c, t) + (double)b * dl * p2p_beta(sys, c, t) * hv;
             }
             o->t_halo = 2.0 * sum;
         }
@@ -892,7 +905,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
             const or_layer *r = &m->rows[l];
             if (r->kind != OR_CONV && r->kind != OR_POOL) continue;
             double hv = (double)(or_halo_elements(r, split, 0) + or_halo_elements(r, split, 1));
-            sum += 2.0 * c->alpha[t] + (double)b * dl * c->beta[t] * hv;
+            sum += 2.0 * p2p_alpha(sys, c, t) + (double)b * dl * p2p_beta(sys, c, t) * hv;
         }
         o->t_halo = 2.0 * sum;
     }
@@ -915,7 +928,7 @@ int or_eval_fold(const or_model *models, const or_system *sys, const or_config *
             mU = U > mU ? U : mU;
             memx = mm > memx ? mm : memx;
             if (i < c->n_stages - 1 && ts >= 0)
-                sumP2P += c->alpha[ts] + dl * (double)b * (double)m->rows[c->stage_end[i] - 1].y * c->beta[ts];
+                sumP2P += p2p_alpha(sys, c, ts) + dl * (double)b * (double)m->rows[c->stage_end[i] - 1].y * p2p_beta(sys, c, ts);
             beg = c->stage_end[i];
         }
         o->mem = sys->gamma * memx;

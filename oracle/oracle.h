@@ -56,6 +56,11 @@ typedef struct {
     or_tier tiers[OR_MAX_TIERS];
     double flops_per_s, hbm_bytes, gamma, phi_df, tree_threshold;
     int32_t tree_chunks, filter_rs;   /* filter_rs: backward dL/dx exchange as Reduce-Scatter (P:355 fn) */
+    /* f1 (Q40): point-to-point patterns (halo exchange, pipeline boundary
+     * sends) use the tier's alpha x p2p_alpha_scale and beta x p2p_beta_scale (e.g. MPI vs
+     * NCCL); phi_pd / phi_ds: contention on the pd stage Allreduces (s > 1 concurrent groups)
+     * and on the ds reduce-to-leader (p1 > 1 concurrent groups).  All 1 = Table 2 literal. */
+    double p2p_alpha_scale, p2p_beta_scale, phi_pd, phi_ds;
 } or_system;
 
 typedef struct {

@@ -18,6 +18,9 @@ CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "
 
 
 def build(force: bool = False) -> str:
+    # PARADL_ORACLE_LIB: a prebuilt oracle (e.g. the ASan/UBSan build of tools/oracle_sanitize.sh)
+    if os.environ.get("PARADL_ORACLE_LIB"):
+        return os.environ["PARADL_ORACLE_LIB"]
     src = os.path.join(HERE, "oracle.c")
     hdr = os.path.join(HERE, "oracle.h")
     if (not force and os.path.exists(LIB_PATH)
@@ -54,7 +57,9 @@ class System(C.Structure):
     _fields_ = [("n_tiers", C.c_int32), ("delta", C.c_int32), ("tiers", Tier * MAX_TIERS),
                 ("flops_per_s", C.c_double), ("hbm_bytes", C.c_double), ("gamma", C.c_double),
                 ("phi_df", C.c_double), ("tree_threshold", C.c_double),
-                ("tree_chunks", C.c_int32), ("filter_rs", C.c_int32)]
+                ("tree_chunks", C.c_int32), ("filter_rs", C.c_int32),
+                ("p2p_alpha_scale", C.c_double), ("p2p_beta_scale", C.c_double),
+                ("phi_pd", C.c_double), ("phi_ds", C.c_double)]
 
 
 class Sub(C.Structure):
@@ -176,6 +181,10 @@ class OracleSweep:
         self.system.tree_threshold = s.tree_threshold
         self.system.tree_chunks = s.tree_chunks
         self.system.filter_rs = s.filter_rs
+        self.system.p2p_alpha_scale = s.p2p_alpha_scale
+        self.system.p2p_beta_scale = s.p2p_beta_scale
+        self.system.phi_pd = s.phi_pd
+        self.system.phi_ds = s.phi_ds
         subs = (Sub * max(1, len(sweep.subs)))()
         for i, sb in enumerate(sweep.subs):
             x = subs[i]

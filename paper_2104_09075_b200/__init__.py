@@ -71,6 +71,10 @@ def make_system(s) -> A.System:
     S.tree_threshold_B = s.tree_threshold
     S.tree_chunks = s.tree_chunks
     S.filter_rs = s.filter_rs
+    S.p2p_alpha_scale = getattr(s, "p2p_alpha_scale", 1.0)
+    S.p2p_beta_scale = getattr(s, "p2p_beta_scale", 1.0)
+    S.phi_pd = getattr(s, "phi_pd", 1.0)
+    S.phi_ds = getattr(s, "phi_ds", 1.0)
     return S
 
 

@@ -30,7 +30,9 @@ class System(C.Structure):
     _fields_ = [("n_tiers", C.c_int32), ("delta", C.c_int32), ("tiers", Tier * MAX_TIERS),
                 ("flops_per_s", C.c_double), ("hbm_bytes", C.c_double), ("gamma", C.c_double),
                 ("phi_df", C.c_double), ("tree_threshold_B", C.c_double),
-                ("tree_chunks", C.c_int32), ("filter_rs", C.c_int32)]
+                ("tree_chunks", C.c_int32), ("filter_rs", C.c_int32),
+                ("p2p_alpha_scale", C.c_double), ("p2p_beta_scale", C.c_double),
+                ("phi_pd", C.c_double), ("phi_ds", C.c_double)]
 
 
 class SubSweep(C.Structure):

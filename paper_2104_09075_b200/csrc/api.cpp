@@ -283,6 +283,10 @@ extern "C" paradl_status paradl_set_system(paradl_ctx *c, const paradl_system *s
     if (!(std::isfinite(s->tree_threshold_B) && s->tree_threshold_B >= 0.0) || s->tree_chunks < 1)
         return fail(c, PARADL_EINVAL, "tree_threshold >= 0 and tree_chunks >= 1 required");
     if (s->filter_rs != 0 && s->filter_rs != 1) return fail(c, PARADL_EINVAL, "filter_rs must be 0 or 1");
+    if (!finite_pos(s->p2p_alpha_scale) || !finite_pos(s->p2p_beta_scale))
+        return fail(c, PARADL_EINVAL, "p2p scales must be > 0");
+    if (!(std::isfinite(s->phi_pd) && s->phi_pd >= 1.0) || !(std::isfinite(s->phi_ds) && s->phi_ds >= 1.0))
+        return fail(c, PARADL_EINVAL, "phi_pd and phi_ds must be >= 1");
     c->sys = *s;
     c->have_system = true;
     c->img_epoch = ~0ull;
@@ -348,6 +352,9 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
     if (!c->have_system) return fail(c, PARADL_ESTATE, "paradl_set_system not called");
     const paradl_system &sy = c->sys;
     const int NT = sy.n_tiers;
+    // image tiers: the collective tiers, plus their point-to-point copies when the p2p
+    // scales are not 1 (Q40; one IEEE product per value, the oracle forms the same product)
+    const int NTI = (sy.p2p_alpha_scale != 1.0 || sy.p2p_beta_scale != 1.0) ? 2 * NT : NT;
     // value tables are appended after the headers
     std::vector<uint8_t> tab;
     auto put = [&](const void *src, size_t bytes) -> uint32_t {
@@ -429,6 +436,20 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         else for (int t = 0; t < NT; t++) be.push_back(sy.tiers[t].beta_s_per_B);
         for (double v : al) if (!(std::isfinite(v) && v >= 0.0)) return fail(c, PARADL_EINVAL, "sub %d: alpha must be >= 0", i);
         for (double v : be) if (!finite_pos(v)) return fail(c, PARADL_EINVAL, "sub %d: beta must be > 0", i);
+        if (NTI != NT) {
+            // point-to-point copies of every row (Q40): [the NT tier values | each x its p2p scale]
+            std::vector<double> al2, be2;
+            for (size_t r = 0; r < al.size() / NT; r++) {
+                for (int t = 0; t < NT; t++) al2.push_back(al[r * NT + t]);
+                for (int t = 0; t < NT; t++) al2.push_back(al[r * NT + t] * sy.p2p_alpha_scale);
+            }
+            for (size_t r = 0; r < be.size() / NT; r++) {
+                for (int t = 0; t < NT; t++) be2.push_back(be[r * NT + t]);
+                for (int t = 0; t < NT; t++) be2.push_back(be[r * NT + t] * sy.p2p_beta_scale);
+            }
+            al.swap(al2);
+            be.swap(be2);
+        }
         // partition radix
         uint64_t part_n = 1;
         h.part_mode = s.part_mode;
@@ -496,8 +517,8 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
         h.family = fam;
         h.model = mi;
         h.G = G;
-        h.radix[D_BETA] = (uint32_t)(be.size() / NT);
-        h.radix[D_ALPHA] = (uint32_t)(al.size() / NT);
+        h.radix[D_BETA] = (uint32_t)(be.size() / NTI);
+        h.radix[D_ALPHA] = (uint32_t)(al.size() / NTI);
         h.radix[D_LS] = (uint32_t)Ll.size();
         h.radix[D_DIMS] = (uint32_t)(dl.size() / 4);
         h.radix[D_S] = (uint32_t)Sl.size();
@@ -539,7 +560,11 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
     ImgHdr H{};
     H.n_sub = (int32_t)P.subs.size();
     H.n_models = (int32_t)P.model_ids.size();
-    H.n_tiers = NT;
+    H.n_tiers = NTI;
+    H.n_ctiers = NT;
+    H.p2p_off = NTI == NT ? 0 : NT;
+    H.phi_pd = sy.phi_pd;
+    H.phi_ds = sy.phi_ds;
     H.delta = sy.delta;
     H.tree_chunks = sy.tree_chunks;
     H.ar_mult = sy.filter_rs ? 1.0 : 2.0;

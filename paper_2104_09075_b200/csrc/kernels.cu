@@ -103,10 +103,13 @@ __device__ __forceinline__ View make_view(const uint8_t *img, int sub) {
 }
 
 __device__ __forceinline__ int tier_of(const ImgHdr *H, int64_t span) {
-    for (int t = 0; t < H->n_tiers; t++)
+    for (int t = 0; t < H->n_ctiers; t++)
         if (H->max_pes[t] >= span) return t;
     return -1;
 }
+
+// alpha/beta column of the point-to-point copy of tier t (Q40); t < 0 stays < 0
+__device__ __forceinline__ int p2p_tier(const ImgHdr *H, int t) { return t < 0 ? t : t + H->p2p_off; }
 
 __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -505,7 +508,8 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.h_on = p2 > 1;
         m.h_na = i2d(2 * NS);
         m.h_s = i2d(b * delta * HV);
-        m.h_t = ti;
+        m.h_t = p2p_tier(H, ti);
+        if (FAM == PARADL_DS) m.phi = p1 > 1 ? H->phi_ds : 1.0;   // concurrent reduce-to-leader (Q40)
         if (FAM == PARADL_SPATIAL) {
             m.ge = make_ar(H, p, i2d(dW), div_i(dW, p), to);
         } else {
@@ -553,7 +557,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
         m.h_on = p > 1;
         m.h_na = i2d(2 * NS);
         m.h_s = i2d(b * delta * HV);
-        m.h_t = t;
+        m.h_t = p2p_tier(H, t);
         m.ge = make_ar(H, p, i2d(dW), div_i(dW, p), t);
         m.ag_on = Lp < M->G && p > 1;
         m.ag_c = i2d(p - 1);
@@ -579,7 +583,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.bS_memo = div_i(b, Sg);
         }
         m.comp = 0.0;
-        m.pp_t = ts;
+        m.pp_t = p2p_tier(H, ts);
         m.gS = (int)Sg;
         m.gns = ns;
         m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
@@ -705,7 +709,7 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.pp_on = ns > 1;
             m.pp_na = i2d(ns - 1);
             m.pp_s = i2d(delta * b * st.sumY);
-            m.pp_t = ts;
+            m.pp_t = p2p_tier(H, ts);
         } else {
             if (b != m.bS_b || Sg != m.bS_S) {
                 m.bS_b = b;
@@ -718,12 +722,13 @@ __device__ void compute_mid(const View &v, const Lane &L, const StageT &st, Mid 
             m.pp_on = ns > 1;
             m.pp_c = i2d(2 * (ns + Sg - 2));
             m.pp_s = dmul(bS, i2d(delta * st.maxY));
-            m.pp_t = ts;
+            m.pp_t = p2p_tier(H, ts);
             if (FAM == PARADL_PD) {
                 const int tp = tier_of(H, p);
                 reason |= flag_tier(tp);
                 const double mW = i2d(delta * st.maxW);
                 m.ge = make_ar(H, pd, mW, div_i(delta * st.maxW, pd), tp);
+                m.phi = ns > 1 ? H->phi_pd : 1.0;   // the s stage Allreduces at once (Q40)
             }
         }
         m.mem = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
@@ -959,8 +964,12 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
         const double bh = use_phi ? dmul(brow[r.t], phi) : brow[r.t];
         return dmul(r.c, dadd(arow[r.t], dmul(r.s, bh)));
     };
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_SPATIAL_AG) {
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_SPATIAL_AG) {
         ge = ar_eval(m.ge, 1.0, false);
+        if (m.ge.on) t = dadd(t, ge);
+    }
+    if (FAM == PARADL_PD) {
+        ge = ar_eval(m.ge, m.phi, true);
         if (m.ge.on) t = dadd(t, ge);
     }
     if (FAM == PARADL_SPATIAL_AG && m.ag_on) {   // boundary Allgather
@@ -969,7 +978,7 @@ __device__ __forceinline__ double inner(const Mid &m, const double *arow, const 
         t = dadd(t, ag);
     }
     if (FAM == PARADL_DS) {
-        ge = dadd(ar_eval(m.ge, 1.0, false), ar_eval(m.ge2, 1.0, false));
+        ge = dadd(ar_eval(m.ge, m.phi, true), ar_eval(m.ge2, 1.0, false));
         t = dadd(t, ge);
     }
     if (FAM == PARADL_DF) {
@@ -1078,9 +1087,9 @@ __device__ __forceinline__ void alpha_vals(const Mid &m, const double *arow, Alp
 
 template <int FAM>
 __device__ __forceinline__ void slot_vals(const Mid &m, const double *brow, SlotV &v) {
-    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_PD || FAM == PARADL_DS || FAM == PARADL_SPATIAL_AG ||
-        FAM == PARADL_LAYERWISE)
+    if (FAM == PARADL_DATA || FAM == PARADL_SPATIAL || FAM == PARADL_SPATIAL_AG || FAM == PARADL_LAYERWISE)
         v.ge = dmul(m.ge.s, brow[m.ge.t]);
+    if (FAM == PARADL_PD || FAM == PARADL_DS) v.ge = dmul(m.ge.s, dmul(brow[m.ge.t], m.phi));
     if (FAM == PARADL_LAYERWISE) {
         v.ag = dmul(m.ag_s, brow[m.ag_t]);
         v.pp = dmul(m.pp_s, brow[m.pp_t]);
@@ -1855,7 +1864,7 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
         rp = 0;
         ts = tier_of(H, ns);
         rp |= flag_tier(ts);
-        ts = max(ts, 0);
+        ts = max(ts, 0) + H->p2p_off;   // point-to-point column (Q40)
         const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
         if (!(memv <= cap)) rp |= PARADL_R_MEMORY;
         if (FAM == PARADL_LAYERPURE) {
@@ -1878,6 +1887,7 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
         uint32_t rd = rp;
         double ge_c = 0.0, ge_s = 0.0;
         int ge_t = 0;
+        const double ge_phi = ns > 1 ? H->phi_pd : 1.0;   // concurrent stage Allreduces (Q40)
         if (FAM == PARADL_PD && act) {
             const int tp = tier_of(H, ns * pd);
             rd |= flag_tier(tp);
@@ -1913,7 +1923,8 @@ __device__ __forceinline__ void eval_partition(BlkCtx &C, bool act, const Lane &
                     for (uint32_t ib = 0; ib < C.nB; ib++) {
                         const double *brow = C.beta_tab + (size_t)ib * NT;
                         double t = comp;
-                        if (FAM == PARADL_PD) t = dadd(t, dmul(ge_c, dadd(arow[ge_t], dmul(ge_s, brow[ge_t]))));
+                        if (FAM == PARADL_PD)
+                            t = dadd(t, dmul(ge_c, dadd(arow[ge_t], dmul(ge_s, dmul(brow[ge_t], ge_phi)))));
                         if (FAM == PARADL_LAYERPURE)
                             t = dadd(t, dmul(2.0, dadd(aval_pp, dmul(lp_s, brow[ts]))));
                         else
@@ -1974,7 +1985,7 @@ __device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, con
             C.tau = ddiv(1.0, R);
         }
         const int tsr = tier_of(H, ns);
-        ts = max(tsr, 0);
+        ts = max(tsr, 0) + H->p2p_off;   // point-to-point column (Q40)
         const double memv = dmul(H->gamma, dmul(i2d(delta), i2d(st.memI)));
         part_inf = (tsr >= 0 && memv <= cap) ? 0.0 : INF;
         FBs = i2d(st.maxF + st.maxB);
@@ -2035,7 +2046,8 @@ __device__ __forceinline__ void eval_partition_screened(BlkCtx &C, bool act, con
                             const double I = mrow[C.nS + iD];
                             const int gt = gt_row[iD];
                             const double G =
-                                dmul(gc_row[iD], dadd(arow[gt], dmul(gs_tab[(size_t)iD * kThreads], brow[gt])));
+                                dmul(gc_row[iD], dadd(arow[gt], dmul(gs_tab[(size_t)iD * kThreads],
+                                                                     dmul(brow[gt], ns > 1 ? H->phi_pd : 1.0))));
 #pragma unroll
                             for (int u = 0; u < kSB; u++)
                                 hmin = min(hmin, __double2hiint(dmul(dadd(dadd(comp[u], G), P[u]), I)));
@@ -2760,7 +2772,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
             const uint32_t ia1 = nA > 1 ? 1 : 0, ib1 = nBt > 1 ? 1 : 0;
             for (uint32_t n = threadIdx.x; n < ns1; n += blockDim.x) {
                 const int t = n >= 1 ? tier_of(v.H, n) : -1;
-                const int tt = max(t, 0);
+                const int tt = max(t, 0) + v.H->p2p_off;   // point-to-point column (Q40)
                 CmbN q;
                 q.a0 = al[tt];
                 q.a1 = al[ia1 * NT + tt];
@@ -2796,8 +2808,11 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 q.gc = tp < 0 ? CUDART_INF : (pd != 1 ? i2d(2 * (pd - 1)) : 0.0);
                 q.a0 = al[tt];
                 q.a1 = al[ia1 * NT + tt];
-                q.b0 = be[tt];
-                q.b1 = be[ib1 * NT + tt];
+                // beta x phi_pd when the n stage Allreduces run at once (Q40): the oracle's
+                // beta * phi product, formed once here instead of per configuration
+                const double phi = (w.family == PARADL_PD && n > 1) ? v.H->phi_pd : 1.0;
+                q.b0 = dmul(be[tt], phi);
+                q.b1 = dmul(be[ib1 * NT + tt], phi);
                 const bool pow2 = pd > 0 && (pd & (pd - 1)) == 0;
                 q.scale = pow2 ? __longlong_as_double((long long)(1023 - (63 - __clzll(pd))) << 52) : 0.0;
                 q.pd = (int32_t)pd;
@@ -2819,8 +2834,8 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 NTab q;
                 q.cseg = dmul(i2d((int64_t)n + Sg - 1), ddiv(i2d(bv[r]), i2d(Sg)));
                 q.ppc = i2d(n > 1 ? 2 * ((int64_t)n + Sg - 2) : 0);
-                q.aw = t >= 0 ? al[t] : 0.0;
-                q.bw = t >= 0 ? be[t] : 0.0;
+                q.aw = t >= 0 ? al[t + v.H->p2p_off] : 0.0;   // point-to-point column (Q40)
+                q.bw = t >= 0 ? be[t + v.H->p2p_off] : 0.0;
                 nt[e] = q;
             }
         }
@@ -3291,9 +3306,10 @@ __global__ void explain_kernel(const uint8_t *img, int32_t sub, uint64_t local, 
     cfg->Ls = at<int32_t>(img, S->off_Ls)[L.d[D_LS]];
     for (int a = 0; a < 4; a++) cfg->dims[a] = at<int32_t>(img, S->off_dims)[4 * L.d[D_DIMS] + a];
     const int NT = v.H->n_tiers;
-    for (int t = 0; t < PARADL_MAX_TIERS; t++) {
-        cfg->alpha[t] = t < NT ? at<double>(img, S->off_alpha)[(size_t)L.d[D_ALPHA] * NT + t] : 0.0;
-        cfg->beta[t] = t < NT ? at<double>(img, S->off_beta)[(size_t)L.d[D_BETA] * NT + t] : 0.0;
+    for (int t = 0; t < PARADL_MAX_TIERS; t++) {   // the collective tiers
+        const bool in = t < v.H->n_ctiers;
+        cfg->alpha[t] = in ? at<double>(img, S->off_alpha)[(size_t)L.d[D_ALPHA] * NT + t] : 0.0;
+        cfg->beta[t] = in ? at<double>(img, S->off_beta)[(size_t)L.d[D_BETA] * NT + t] : 0.0;
     }
     {
         const int G = v.M->G;

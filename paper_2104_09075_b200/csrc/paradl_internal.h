@@ -59,7 +59,10 @@ struct ImgHdr {
     int32_t delta, tree_chunks;
     double gamma, phi_df, tree_thr;
     double ar_mult;                    // filter/channel/df FB-AR = ar_mult x FB-AG: 2 (Allreduce), 1 (Reduce-Scatter)
-    double pad_hdr;
+    double phi_pd, phi_ds;             // contention on the pd stage Allreduces (s > 1), ds reduce-to-leader (p1 > 1)
+    // tiers: n_ctiers collective tiers (tier_of scans these); alpha/beta rows hold n_tiers values,
+    // the point-to-point copies (x p2p scales) at p2p_off + t when the scales are not 1 (Q40)
+    int32_t n_ctiers, p2p_off;
     int64_t max_pes[PARADL_MAX_TIERS];
     uint32_t model_off[kMaxModelsPerSweep];
     uint32_t sub_off[kMaxSub];

@@ -111,6 +111,10 @@ def exact(sweep, cfg):
     dl = sys.delta
     A = [Fr(v) for v in cfg["alpha"]]
     Bt = [Fr(v) for v in cfg["beta"]]
+    # point-to-point patterns (Q40): the tier's parameters times the p2p scales, each product
+    # rounded to double as the system would hold it
+    Ap = [Fr(float(v) * sys.p2p_alpha_scale) for v in cfg["alpha"]]
+    Bp = [Fr(float(v) * sys.p2p_beta_scale) for v in cfg["beta"]]
     gamma = Fr(sys.gamma)
     p1, d1, d2, d3 = cfg["dims"]
     reason = 0
@@ -168,11 +172,13 @@ def exact(sweep, cfg):
         ti, to = tier(p2), tier(p)
         if p2 > 1:
             halo = inf if ti is None else 2 * sum(
-                2 * A[ti] + b * dl * Bt[ti] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
+                2 * Ap[ti] + b * dl * Bp[ti] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
         if fam == W.SPATIAL:
             ge = inf if to is None else ar_exact(sys, p, Fr(dl * W_), Fr(dl * W_, p), A[to], Bt[to])
         else:
-            rl = inf if ti is None else ar_exact(sys, p2, Fr(dl * W_), Fr(dl * W_, p2), A[ti], Bt[ti])
+            phi = Fr(float(cfg["beta"][ti]) * sys.phi_ds) if (ti is not None and p1 > 1) else None
+            rl = inf if ti is None else ar_exact(sys, p2, Fr(dl * W_), Fr(dl * W_, p2), A[ti],
+                                                 phi if phi is not None else Bt[ti])
             al = inf if to is None else ar_exact(sys, p1, Fr(dl * W_), Fr(dl * W_, p1), A[to], Bt[to])
             ge = inf if (rl is None or al is None) else rl + al
         mem = mem_row(B, p, 1)
@@ -255,7 +261,7 @@ def exact(sweep, cfg):
         t = tier(p)
         if p > 1:
             halo = inf if t is None else 2 * sum(
-                2 * A[t] + b * dl * Bt[t] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
+                2 * Ap[t] + b * dl * Bp[t] * (halo_rows(r, split, 0) + halo_rows(r, split, 1)) for r in Sp)
             if Lp < len(L):
                 ag = inf if t is None else (p - 1) * (A[t] + Fr(B * L[Lp - 1].y, p) * dl * Bt[t])
         ge = inf if t is None else ar_exact(sys, p, Fr(dl * W_), Fr(dl * W_, p), A[t], Bt[t])
@@ -322,7 +328,7 @@ def exact(sweep, cfg):
             if ts is None:
                 comp = inf
             else:
-                c = [A[ts] + mb * dl * y * Bt[ts] for y in ycut] + [Fr(0)]
+                c = [Ap[ts] + mb * dl * y * Bp[ts] for y in ycut] + [Fr(0)]
                 d = [mb * FWg[i] + c[i] for i in range(s)]
                 e = [mb * BWg[i] + (c[i - 1] if i > 0 else 0) for i in range(s)]
                 t_f = sum(d) + (S - 1) * max(d)
@@ -330,18 +336,19 @@ def exact(sweep, cfg):
         elif fam == W.LAYERPURE:
             comp = comp_row(b, 1, 1)
             if s > 1:
-                p2p = inf if ts is None else 2 * sum(A[ts] + dl * b * y * Bt[ts] for y in ycut)
+                p2p = inf if ts is None else 2 * sum(Ap[ts] + dl * b * y * Bp[ts] for y in ycut)
         else:
             comp = Fr(s + S - 1, S) * b * (max(FWg) + max(BWg)) + max(WUg)
             if s > 1:
-                p2p = inf if ts is None else 2 * (s + S - 2) * max(A[ts] + Fr(b, S) * y * dl * Bt[ts] for y in ycut)
+                p2p = inf if ts is None else 2 * (s + S - 2) * max(Ap[ts] + Fr(b, S) * y * dl * Bp[ts] for y in ycut)
             if fam == W.PD:
                 tp = tier(p)
                 if tp is None:
                     ge = inf if pd > 1 else Fr(0)
                 else:
                     mW = dl * max(Wg)
-                    ge = ar_exact(sys, pd, Fr(mW), Fr(mW, pd), A[tp], Bt[tp])
+                    bh = Fr(float(cfg["beta"][tp]) * sys.phi_pd) if s > 1 else Bt[tp]
+                    ge = ar_exact(sys, pd, Fr(mW), Fr(mW, pd), A[tp], bh)
         mem = gamma * dl * max(sum(2 * b * (r.x + r.y) + 2 * r.w + r.bi for r in g) for g in groups)
         if S < 1 or S > b:
             reason |= R_SEGMENTS
@@ -415,6 +422,35 @@ def concurrent_rings_sim(group_bytes, p, alpha, beta):
         col = [sum((i + 1) * 1000 + c + 7 * g for i in range(p)) for c in range(p)]
         assert all(row == col for row in acc)
     return max(clock)
+
+
+def contended_stage_rings_sim(s, pd, node, m_bytes, alpha, beta):
+    """pd gradient exchange with contention (Q40): PEs numbered replica-major (PE =
+    r s + i for stage i of replica r), `node` PEs per node; stage i's ring Allreduce runs
+    over PEs i, s + i, ..., (pd - 1) s + i, all s rings at once and in lockstep.  Every ring
+    step sends one m/pd segment from each member to the next; a directed inter-node link
+    carrying f flows gives each flow 1/f of its bandwidth (beta x f), so a step lasts
+    alpha + seg beta (the busiest link's flow count).  Returns (makespan, flows on the busiest
+    link) in exact rationals -- the contention coefficient phi is counted, not assumed."""
+    if pd == 1:
+        return Fr(0), 0
+    seg = Fr(m_bytes, pd)
+    t = Fr(0)
+    worst = 0
+    for step in range(2 * (pd - 1)):
+        flows = {}
+        msgs = []
+        for i in range(s):
+            for r in range(pd):
+                a, b = r * s + i, ((r + 1) % pd) * s + i
+                na, nb = a // node, b // node
+                msgs.append((i, na, nb))
+                if na != nb:
+                    flows[(na, nb)] = flows.get((na, nb), 0) + 1
+        f = max(flows.values(), default=1)
+        worst = max(worst, f)
+        t += alpha + seg * beta * f
+    return t, worst
 
 
 def ring_allgather_sim(p, m_seg, alpha, beta):

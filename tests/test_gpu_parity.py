@@ -672,3 +672,36 @@ def test_full_sweep_chunks_vs_oracle_golden(dev, cfg):
         assert [h[1] for h in hits[:len(gh)]] == [float.fromhex(k) for _, k in gh]
         done += 1
     assert done > 0
+
+
+# ------------------------------------------------------------------ f1: per-pattern parameters, contention
+@pytest.mark.parametrize("cfg,kw", [(5, dict(s_max=3)), (2, dict(n_alpha=3, n_beta=32, b_list=[2, 64], pipe_smax=3)),
+                                    (4, dict(n_alpha=2, n_beta=32)), (3, dict(n_alpha=2, n_beta=3))])
+def test_p2p_scales_and_contention_all_paths(dev, oracle_mod, cfg, kw):
+    """DESIGN.md Q40: point-to-point alpha/beta scales and the pd / ds
+    contention coefficients through every evaluation path (mode-3 COMB pd, mode-0 slots,
+    structure-free dense, mode-2 masks) against the oracle: whole-sweep top-64 + count,
+    dense windows, and ragged windows."""
+    import dataclasses
+    sw = W.CONFIGS[cfg](**kw)
+    sw.system = dataclasses.replace(sw.system, p2p_alpha_scale=2.5, p2p_beta_scale=1.75, phi_pd=2.0, phi_ds=3.0)
+    if cfg == 3:   # a small mask sweep (VGG16's first 14 rows) for the mode-2 path
+        from workloads import models as M
+        vgg = M.vgg16()
+        m = M.Model("vgg14", vgg.layers[:14], vgg.D, default_Ls=14)
+        sw.models = [m]
+        sw.subs = [W.SubSweep(W.PIPELINE, part_mode=W.PART_MASK, S=[4], b=[64]),
+                   W.SubSweep(W.PIPELINE, part_mode=W.PART_MASK, S=[2], b=[8, 64], alpha=sw.subs[0].alpha[:1],
+                              beta=sw.subs[0].beta[:2])]
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    check_topk(ctx, spec, osw, 0, n, 64)
+    rng = random.Random(cfg)
+    for _ in range(4):
+        a = rng.randrange(n)
+        c = min(n - a, rng.randrange(1, 200_000))
+        check_topk(ctx, spec, osw, a, c, 16)
+        c = min(c, 20_000)
+        assert check_dense(ctx, spec, osw, a, c, dev) == 0

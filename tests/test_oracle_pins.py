@@ -365,6 +365,70 @@ def test_layerwise_transitions_are_ring_collectives(oracle_mod):
     assert _rel(back.t_fb_ag, ag_fc2 + ag_in) <= 4e-16
 
 
+@pytest.mark.parametrize("s,pd,node", [(2, 4, 4), (3, 2, 6), (4, 8, 8), (2, 2, 2), (1, 8, 4)])
+def test_pd_ge_contention_equals_flow_count(oracle_mod, s, pd, node):
+    """f1 contention (P:561 'divides the bandwidth of a link by the number of communication
+    flows'; Q40): the s stage Allreduces of pd share the inter-node links; a link-level
+    simulation of the concurrent rings counts the flows on the busiest link, and the oracle
+    with phi_pd = that count gives the simulated makespan (s = 1: a single ring, no phi)."""
+    a, be = 4e-6, 1.0 / 11e9
+    ws = [4096 * (i + 1) for i in range(s)]
+    rows = [toys.row(w=w, fw=1, bw=1, y=1) for w in ws]
+    m = toys.model(rows)
+    want, flows = brute.contended_stage_rings_sim(s, pd, node, 4 * max(ws), Fr(a), Fr(be))
+    sysd = toys.system(alpha=a, beta=be, delta=4)
+    sysd.phi_pd = float(max(flows, 1)) if s > 1 else 7.0   # s = 1 must ignore phi_pd
+    pr = _one(oracle_mod, m, sysd, W.SubSweep(W.PD, b=[8], S=[1], dims=[(pd, 1, 1, 1)], part_mode=W.PART_COMB,
+                                              s_min=s, s_max=s))
+    assert _rel(pr.t_ge, want) <= 4e-16
+    if s > 1:   # replica-major layout: every stage ring crosses the same inter-node links
+        assert flows == (s if s * pd > node else 1)
+
+
+def test_p2p_scales_touch_point_to_point_patterns_only(oracle_mod):
+    """f1 per-pattern parameters (P:768-769 'different network parameters ... for MPI and
+    NCCL'; Q40): with p2p scales (ka, kb) the halo exchange and the pipeline boundary sends
+    equal those of a system whose tiers are (alpha ka, beta kb), while every collective
+    (GE Allreduce, filter Allgather) equals the unscaled system's; and a 2-stage pipeline's
+    boundary term is 2 (S) Hockney sends T_p2p(m) = alpha' + m beta'."""
+    import dataclasses
+    ka, kb = 3.0, 2.5
+    a, be = 2e-6, 1.0 / 8e9
+    spat = toys.model([toys.row(kind=M.CONV, C=4, F=4, X=(16, 16, 1), Y=(16, 16, 1), K=(3, 3, 1), x=1024,
+                                y=1024, w=144, fw=10, bw=20)], Ls=1)
+    base = toys.system(alpha=a, beta=be, delta=4)
+    scaled = dataclasses.replace(base, p2p_alpha_scale=ka, p2p_beta_scale=kb)
+    shifted = toys.system(alpha=a * ka, beta=be * kb, delta=4)
+    sub = W.SubSweep(W.SPATIAL, b=[2], dims=[(1, 2, 2, 1)], Ls=[1])
+    x, y, z = (_one(oracle_mod, spat, sd, sub) for sd in (scaled, shifted, base))
+    assert x.t_halo == y.t_halo and x.t_halo != z.t_halo
+    assert x.t_ge == z.t_ge and x.t_ge != y.t_ge
+    pipe = toys.model([toys.row(y=5000, fw=10, bw=20), toys.row(y=3, fw=10, bw=20)])
+    S, b = 2, 4
+    pr = _one(oracle_mod, pipe, scaled, W.SubSweep(W.PIPELINE, b=[b], S=[S], part_mode=W.PART_COMB, s_min=2, s_max=2))
+    send = Fr(a * ka) + Fr(b, S) * 5000 * 4 * Fr(be * kb)        # T_p2p(m) = alpha + m beta
+    assert _rel(pr.t_p2p, 2 * (2 + S - 2) * send) <= 4e-16
+    filt = toys.model([toys.row(y=64, F=64), toys.row(F=64)])
+    fs = W.SubSweep(W.FILTER, b=[2], dims=[(4, 1, 1, 1)])
+    assert _one(oracle_mod, filt, scaled, fs).t_fb_ag == _one(oracle_mod, filt, base, fs).t_fb_ag
+
+
+def test_ds_reduce_to_leader_contention(oracle_mod):
+    """phi_ds (Q40) multiplies the beta part of the ds reduce-to-leader only, and only when
+    p1 > 1 groups reduce at once; the leaders' Allreduce and ds(1; split) are unchanged."""
+    import dataclasses
+    m = toys.model([toys.row(w=8192, X=(64, 1, 1), Y=(64, 1, 1))], Ls=0)
+    base = toys.system(alpha=0.0, beta=1e-9)
+    sub = W.SubSweep(W.DS, b=[1], dims=[(4, 2, 1, 1), (1, 2, 1, 1)], Ls=[0])
+    o0 = oracle_mod.OracleSweep(toys.sweep(m, base, [sub]))
+    o2 = oracle_mod.OracleSweep(toys.sweep(m, dataclasses.replace(base, phi_ds=2.0), [sub]))
+    g0, g2 = o0.explain(0), o2.explain(0)
+    al = 2 * (4 - 1) * (8192 / 4) * 1e-9          # leaders' Allreduce, alpha = 0
+    rl = 2 * (2 - 1) * (8192 / 2) * 1e-9           # reduce-to-leader
+    assert _rel(g0.t_ge, rl + al) <= 1e-15 and _rel(g2.t_ge, 2 * rl + al) <= 1e-15
+    assert o0.explain(1).t_ge == o2.explain(1).t_ge
+
+
 def test_partition_balanced_example(oracle_mod):
     e = EX["partition_balanced"]
     m = toys.model([toys.row(fw=c, bw=0) for c in e["costs"]], D=1)

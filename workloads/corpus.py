@@ -53,7 +53,7 @@ def random_system(seed: int) -> W.System:
     nt = rng.randint(1, 3)
     pes = sorted(rng.sample([2, 4, 8, 16, 64, 256, 1024], nt))
     tiers = [W.Tier(pe, rng.uniform(1e-7, 1e-4), 1.0 / rng.uniform(1e9, 1e12)) for pe in pes]
-    return W.System(tiers=tiers,
+    sysd = W.System(tiers=tiers,
                     flops_per_s=rng.choice([1e12, 15.7e12, 37e12, 3.3e11]),
                     hbm_bytes=rng.choice([2.0 ** 20, 2.0 ** 26, 16 * W.GiB]),
                     delta=rng.choice([2, 4, 8]),
@@ -62,6 +62,14 @@ def random_system(seed: int) -> W.System:
                     tree_threshold=rng.choice([0.0, 0.0, 4096.0, 1e6]),
                     tree_chunks=rng.choice([1, 2, 4]),
                     filter_rs=rng.choice([0, 1]))
+    # f1 parameters (Q40), drawn after the others so earlier draws keep their values
+    if rng.random() < 0.5:
+        sysd.p2p_alpha_scale = rng.choice([1.0, 3.0, 0.7])
+        sysd.p2p_beta_scale = rng.choice([1.0, 2.5, 1.3])
+    if rng.random() < 0.5:
+        sysd.phi_pd = rng.choice([1.0, 2.0, 3.0])
+        sysd.phi_ds = rng.choice([1.0, 2.0, 4.0])
+    return sysd
 
 
 def random_sweep(seed: int, max_list: int = 3) -> W.Sweep:

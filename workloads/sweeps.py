@@ -51,6 +51,13 @@ class System:
     tree_threshold: float = 0.0     # bytes; 0 => ring everywhere (Table 2 literal)
     tree_chunks: int = 1
     filter_rs: int = 0              # 1: filter/channel backward exchange as Reduce-Scatter (P:355 fn)
+    # point-to-point patterns (halo, pipeline sends) on their own
+    # alpha/beta (the tier's times these scales, e.g. MPI vs NCCL); contention on
+    # the pd stage Allreduces and the ds reduce-to-leader.  1.0 = Table 2 literal.
+    p2p_alpha_scale: float = 1.0
+    p2p_beta_scale: float = 1.0
+    phi_pd: float = 1.0
+    phi_ds: float = 1.0
 
 
 @dataclass
