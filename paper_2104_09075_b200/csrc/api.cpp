@@ -16,9 +16,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "paradl_internal.h"
 
 using namespace paradl;
+
+// NVTX ranges around every evaluating entry point (header-only NVTX v3: a no-op unless a
+// profiler such as nsys / ncu --nvtx injects itself)
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace
 
 namespace {
 
@@ -204,6 +217,7 @@ static paradl_status validate_row(paradl_ctx *c, const paradl_layer &r, int l) {
 
 extern "C" paradl_status paradl_load_model(paradl_ctx *c, const paradl_layer *rows, int32_t G, int64_t D,
                                            int32_t *model_id) {
+    NvtxRange nvtx_("paradl_load_model");
     if (!c) return PARADL_EINVAL;
     if (!rows || G < 1 || !model_id) return fail(c, PARADL_EINVAL, "need rows, G >= 1 and model_id");
     if (G > 4096) return fail(c, PARADL_EINVAL, "G > 4096 rows is not supported");
@@ -951,13 +965,14 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             a.dtab_bytes = 0;   // unscreened path
         }
         smems[li] = smem + a.memo_bytes + a.low_bytes + a.dtab_bytes;
-        const uint64_t okey = ((uint64_t)fam_of[li] << 40) | ((uint64_t)dense << 39) | ((uint64_t)blk_of[li] << 36) |
+        const uint64_t okey = ((uint64_t)fam_of[li] << 40) | ((uint64_t)(dense ? (cmp ? 2 : 1) : 0) << 38) |
+                              ((uint64_t)blk_of[li] << 35) |
                               (uint64_t)smems[li];
         int nb = -1;
         for (auto &kv : c->occ_cache)
             if (kv.first == okey) nb = kv.second;
         if (nb < 0) {
-            nb = max_blocks_per_sm(fam_of[li], dense, blk_of[li], smems[li]);
+            nb = max_blocks_per_sm(fam_of[li], dense ? (cmp ? 2 : 1) : 0, blk_of[li], smems[li]);
             c->occ_cache.push_back({okey, nb});
         }
         if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smems[li]);
@@ -972,8 +987,10 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
                 const uint64_t nblk = range / (w.mode == 2 ? Q << 8 : Q);
-                // >= ~8 tiles per warp of this rank's shard; 1..256 partitions per lane per tile
-                uint64_t cper = nblk / n_shards / (32ull * warps * 8ull);
+                // >= ~16 tiles per warp of this rank's shard (the last wave of a dynamic tile queue
+                // leaves at most one tile per warp unbalanced: <= ~6 % at 8 shards of cfg5);
+                // 1..256 partitions per lane per tile
+                uint64_t cper = nblk / n_shards / (32ull * warps * 16ull);
                 cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
                 w.steps = (uint32_t)cper;
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
@@ -1105,7 +1122,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             ls = c->streams[li];
             CUDA_TRY(c, cudaStreamWaitEvent(ls, c->fork_ev, 0));
         }
-        CUDA_TRY(c, launch_sweep(fam_of[li], dense, blk_of[li], a, grids[li], smems[li], ls));
+        CUDA_TRY(c, launch_sweep(fam_of[li], dense ? (cmp ? 2 : 1) : 0, blk_of[li], a, grids[li], smems[li], ls));
         c->stat_launches++;
         if (fork) CUDA_TRY(c, cudaEventRecord(c->events[li], ls));
         cta_off += grids[li];
@@ -1124,6 +1141,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
 
 extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
                                       const paradl_dense_out *out, void *stream) {
+    NvtxRange nvtx_("paradl_sweep");
     paradl_status s = need_device(c);
     if (s) return s;
     if (!out) return fail(c, PARADL_EINVAL, "null dense output");
@@ -1142,6 +1160,7 @@ extern "C" paradl_status paradl_sweep(paradl_ctx *c, const paradl_sweep_spec *sp
 
 extern "C" paradl_status paradl_sweep_compact(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first,
                                               uint64_t count, const paradl_compact_out *out, void *stream) {
+    NvtxRange nvtx_("paradl_sweep_compact");
     paradl_status s = need_device(c);
     if (s) return s;
     if (!out || !out->idx || !out->n_feasible) return fail(c, PARADL_EINVAL, "null compact output");
@@ -1168,6 +1187,7 @@ extern "C" paradl_status paradl_sweep_compact(paradl_ctx *c, const paradl_sweep_
 extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
                                            int32_t shard, int32_t n_shards, int32_t k, paradl_hit *d_hits,
                                            uint64_t *d_n_feasible, void *stream) {
+    NvtxRange nvtx_("paradl_topk_async");
     paradl_status s = need_device(c);
     if (s) return s;
     if (k < 1 || k > PARADL_MAX_TOPK) return fail(c, PARADL_EINVAL, "k must be in 1..%d", PARADL_MAX_TOPK);
@@ -1216,6 +1236,7 @@ extern "C" paradl_status paradl_topk_async(paradl_ctx *c, const paradl_sweep_spe
 extern "C" paradl_status paradl_merge_topk(paradl_ctx *c, const paradl_hit *d_lists, int32_t n_lists, int32_t k,
                                            const uint64_t *d_counts, paradl_hit *d_out, uint64_t *d_count_out,
                                            void *stream) {
+    NvtxRange nvtx_("paradl_merge_topk");
     paradl_status s = need_device(c);
     if (s) return s;
     if (k < 1 || k > PARADL_MAX_TOPK || n_lists < 0 || (n_lists && (!d_lists || !d_counts)) || !d_out || !d_count_out)
@@ -1228,6 +1249,7 @@ extern "C" paradl_status paradl_merge_topk(paradl_ctx *c, const paradl_hit *d_li
 
 extern "C" paradl_status paradl_merge_records(paradl_ctx *c, const paradl_hit *d_records, int32_t n_records,
                                               int32_t k, paradl_hit *d_out, uint64_t *d_count_out, void *stream) {
+    NvtxRange nvtx_("paradl_merge_records");
     paradl_status s = need_device(c);
     if (s) return s;
     if (k < 1 || k > PARADL_MAX_TOPK || n_records < 0 || (n_records && !d_records) || !d_out || !d_count_out)
@@ -1241,6 +1263,7 @@ extern "C" paradl_status paradl_merge_records(paradl_ctx *c, const paradl_hit *d
 
 extern "C" paradl_status paradl_topk(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
                                      int32_t k, paradl_hit *hits, uint64_t *n_feasible, void *stream) {
+    NvtxRange nvtx_("paradl_topk");
     paradl_status s = need_device(c);
     if (s) return s;
     if (!hits || !n_feasible) return fail(c, PARADL_EINVAL, "null output");
@@ -1260,6 +1283,7 @@ extern "C" paradl_status paradl_topk(paradl_ctx *c, const paradl_sweep_spec *spe
 
 extern "C" paradl_status paradl_argmin(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t first, uint64_t count,
                                        paradl_hit *best, uint64_t *n_feasible, void *stream) {
+    NvtxRange nvtx_("paradl_argmin");
     return paradl_topk(c, spec, first, count, 1, best, n_feasible, stream);
 }
 
@@ -1296,6 +1320,7 @@ extern "C" paradl_status paradl_decode(paradl_ctx *c, const paradl_sweep_spec *s
 
 extern "C" paradl_status paradl_explain(paradl_ctx *c, const paradl_sweep_spec *spec, uint64_t idx,
                                         paradl_prediction *out) {
+    NvtxRange nvtx_("paradl_explain");
     if (!out) return fail(c, PARADL_EINVAL, "null output");
     return explain_impl(c, spec, idx, nullptr, out);
 }

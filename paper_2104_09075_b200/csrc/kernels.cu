@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <mutex>
 
@@ -34,6 +35,27 @@ namespace paradl {
 #endif
 #ifndef PARADL_PIPE_KEYS
 #define PARADL_PIPE_KEYS 16
+#endif
+
+// Device-side bounds checks of the checked build (-DPARADL_CHECKS=1, tools/checked_build.py):
+// a failed check traps, so the call returns PARADL_ECUDA and the test that made it fails.
+// (compute-sanitizer is not available on the GPU pool.)
+#ifndef PARADL_CHECKS
+#define PARADL_CHECKS 0
+#endif
+#if PARADL_CHECKS
+#define PCHECK(c)                                                                                   \
+    do {                                                                                            \
+        if (!(c)) {                                                                                 \
+            printf("PARADL_CHECKS: %s failed at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                              \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define PCHECK(c) \
+    do {          \
+    } while (0)
 #endif
 
 // ------------------------------------------------------------------ fp64 helpers
@@ -146,6 +168,7 @@ __device__ void unrank_comb(const View &v, uint64_t r, Lane &L, uint16_t *cuts, 
             rr -= c;
             val++;
         }
+        PCHECK(val >= 1 && val <= n && (q == 1 || val > cuts[(q - 2) * cs]));
         cuts[(q - 1) * cs] = (uint16_t)val;
     }
     L.ns = s;
@@ -199,6 +222,11 @@ __device__ void decode(const View &v, uint64_t u, Lane &L, uint16_t *cuts, int c
     L.ns = 1;
     if (S->part_mode == PARADL_PART_COMB) unrank_comb(v, L.part, L, cuts, cs);
     else if (S->part_mode == PARADL_PART_MASK) L.ns = __popcll(L.part) + 1;
+#if PARADL_CHECKS
+    for (int i = 0; i < kDigits; i++) PCHECK(i == D_PART || L.d[i] < S->radix[i]);
+    PCHECK(L.part < S->part_n || S->part_n == 0);
+    PCHECK(S->part_mode != PARADL_PART_COMB || (L.ns >= S->s_min && L.ns <= S->s_max));
+#endif
 }
 
 // Adds the lane stride (mixed-radix digits inc[]) to the digit vector; returns the
@@ -1468,6 +1496,7 @@ __device__ __forceinline__ uint64_t struct_index(const View &v, const Lane &L) {
     return s;
 }
 __device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) {
+    PCHECK(s >= w.stab_lo);
     const PipeRec *r = w.stab + (s - w.stab_lo);
     const double4 q = *reinterpret_cast<const double4 *>(r);
     const int2 t = *reinterpret_cast<const int2 *>(&r->reason);
@@ -1480,7 +1509,8 @@ __device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) 
 }
 
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
-template <int FAM, bool DENSE>
+// DENSE: 0 reduce (top-k / count), 1 dense writes, 2 compact writes (paradl_sweep_compact)
+template <int FAM, int DENSE>
 __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
                                           uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, double *dtab,
                                           const double *memo) {
@@ -1550,15 +1580,16 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         // compact mode: pass 1 counts the tile's feasible configurations, pass 2 writes them
         // from the tile's scanned offset (warp ballot + popc of the lanes below)
         uint32_t c_tile = 0;
-        uint64_t c_pos = (DENSE && a.c_off) ? a.c_off[w.tile_base + tile] : 0;
+        uint64_t c_pos = (DENSE == 2 && a.c_off) ? a.c_off[w.tile_base + tile] : 0;
+        PCHECK(w.tile_base + tile < a.total_tiles);
 
         // emits one step (step index jj within the tile) for every lane
         auto emit_dense = [&](bool act, double t_it, bool feas, uint32_t jj) {
-            if (a.c_cnt) {
+            if (DENSE == 2 && a.c_cnt) {
                 c_tile += __popc(__ballot_sync(full, act && feas));
                 return;
             }
-            if (a.c_idx) {
+            if (DENSE == 2) {
                 const unsigned bb = __ballot_sync(full, act && feas);
                 const uint64_t pos = c_pos + __popc(bb & ((1u << lane) - 1u));
                 if (act && feas && pos < a.c_cap) {
@@ -1794,7 +1825,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
             const uint64_t pos_end = g0 + 32ull * nsteps - a.first;
             atomicOr(&a.bits[pos_end >> 5], carry);
         }
-        if (DENSE && a.c_cnt && lane == 0) a.c_cnt[w.tile_base + tile] = c_tile;
+        if (DENSE == 2 && a.c_cnt && lane == 0) a.c_cnt[w.tile_base + tile] = c_tile;
     
 }
 
@@ -2501,6 +2532,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
         st.maxF = st.maxB = st.maxU = st.maxW = st.maxY = st.sumY = st.memI = 0;
         int64_t b = 1;
         if (act) {
+            PCHECK(L.d[D_B] < S->radix[D_B] && L.ns >= 1 && L.ns <= S->s_max && L.part < S->part_n);
             b = bv[L.d[D_B]];
             const int64_t twob = 2 * b;
             if (upd) {
@@ -2561,6 +2593,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 }
                 upd = 0;
             }
+            PCHECK(ns == 1 || (clast >= 1 && clast <= G - 1 && clast > (ns >= 3 ? cuts[(ns - 3) * kThreads] : 0)));
             if (ns == 1) {
                 st.maxF = PF[G] - PF[0];
                 st.maxB = PB[G] - PB[0];
@@ -2900,7 +2933,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
     __syncthreads();
 }
 
-template <int FAM, bool DENSE, int BLK>
+template <int FAM, int DENSE, int BLK>
 __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
                                             : (FAM == PARADL_PIPELINE && !DENSE && BLK == 0) ? PARADL_PIPE_MINB
                                                                                              : PARADL_MINB)
@@ -3625,25 +3658,27 @@ cudaError_t launch_compact_scan(const uint32_t *cnt, uint64_t *off, const Compac
 // ------------------------------------------------------------------ launchers
 size_t sweep_smem_extra() { return sizeof(SmemExtra); }
 
-static void *sweep_fn(int family, bool dense, int blk) {
+static void *sweep_fn(int family, int dense, int blk) {
     if (blk) {
         if (dense) return nullptr;
         switch (family) {
         case PARADL_PIPELINE:
-            return blk == 1   ? (void *)sweep_kernel<PARADL_PIPELINE, false, 1>
-                   : blk == 3 ? (void *)sweep_kernel<PARADL_PIPELINE, false, 3>
-                              : (void *)sweep_kernel<PARADL_PIPELINE, false, 2>;
+            return blk == 1   ? (void *)sweep_kernel<PARADL_PIPELINE, 0, 1>
+                   : blk == 3 ? (void *)sweep_kernel<PARADL_PIPELINE, 0, 3>
+                              : (void *)sweep_kernel<PARADL_PIPELINE, 0, 2>;
         case PARADL_LAYERPURE:
-            return blk == 1 ? (void *)sweep_kernel<PARADL_LAYERPURE, false, 1> : (void *)sweep_kernel<PARADL_LAYERPURE, false, 2>;
+            return blk == 1 ? (void *)sweep_kernel<PARADL_LAYERPURE, 0, 1> : (void *)sweep_kernel<PARADL_LAYERPURE, 0, 2>;
         case PARADL_PD:
-            return blk == 1   ? (void *)sweep_kernel<PARADL_PD, false, 1>
-                   : blk == 3 ? (void *)sweep_kernel<PARADL_PD, false, 3>
-                              : (void *)sweep_kernel<PARADL_PD, false, 2>;
+            return blk == 1   ? (void *)sweep_kernel<PARADL_PD, 0, 1>
+                   : blk == 3 ? (void *)sweep_kernel<PARADL_PD, 0, 3>
+                              : (void *)sweep_kernel<PARADL_PD, 0, 2>;
         default: return nullptr;
         }
     }
-#define PARADL_CASE(F) \
-    case F: return dense ? (void *)sweep_kernel<F, true, 0> : (void *)sweep_kernel<F, false, 0>;
+#define PARADL_CASE(F)                                                                     \
+    case F:                                                                                \
+        return dense == 2 ? (void *)sweep_kernel<F, 2, 0>                                  \
+                          : dense ? (void *)sweep_kernel<F, 1, 0> : (void *)sweep_kernel<F, 0, 0>;
     switch (family) {
         PARADL_CASE(PARADL_SERIAL)
         PARADL_CASE(PARADL_DATA)
@@ -3685,7 +3720,7 @@ static cudaError_t ensure_smem_attr(void *fn, size_t smem) {
     return cudaSuccess;
 }
 
-int max_blocks_per_sm(int family, bool dense, int blk, size_t smem) {
+int max_blocks_per_sm(int family, int dense, int blk, size_t smem) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return 0;
     if (ensure_smem_attr(fn, smem) != cudaSuccess) return 0;
@@ -3694,7 +3729,7 @@ int max_blocks_per_sm(int family, bool dense, int blk, size_t smem) {
     return nb;
 }
 
-cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, int grid, size_t smem,
+cudaError_t launch_sweep(int family, int dense, int blk, const LaunchArgs &a, int grid, size_t smem,
                          cudaStream_t st) {
     void *fn = sweep_fn(family, dense, blk);
     if (!fn) return cudaErrorInvalidValue;

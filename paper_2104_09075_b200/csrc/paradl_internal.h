@@ -189,9 +189,10 @@ struct HaloJobs {
 // launchers implemented in kernels.cu
 cudaError_t launch_prep_model(const paradl_layer *d_rows, int32_t G, int64_t D, uint8_t *d_block,
                               const ModelHdr &layout, cudaStream_t st);
-cudaError_t launch_sweep(int family, bool dense, int blk, const LaunchArgs &a, int grid, size_t smem,
+// dense: 0 reduce, 1 dense writes, 2 compact writes
+cudaError_t launch_sweep(int family, int dense, int blk, const LaunchArgs &a, int grid, size_t smem,
                          cudaStream_t st);
-int max_blocks_per_sm(int family, bool dense, int blk, size_t smem);
+int max_blocks_per_sm(int family, int dense, int blk, size_t smem);
 size_t sweep_smem_extra();
 cudaError_t launch_merge(const paradl_hit *lists, int64_t n_lists, int32_t k,
                          const unsigned long long *counts, int32_t n_counts, paradl_hit *out,

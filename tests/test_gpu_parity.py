@@ -705,3 +705,28 @@ def test_p2p_scales_and_contention_all_paths(dev, oracle_mod, cfg, kw):
         check_topk(ctx, spec, osw, a, c, 16)
         c = min(c, 20_000)
         assert check_dense(ctx, spec, osw, a, c, dev) == 0
+
+
+def test_repeated_and_concurrent_calls_identical(dev):
+    """Race surrogate (compute-sanitizer is unavailable on the pool): a sweep whose top-k uses
+    the fused two-level merge (many CTA lists, last-block ticket) and the shared admission
+    bound gives bit-identical hits and counts over 20 repeated calls, and when two contexts
+    run it at once on two streams."""
+    sw = W.config2(n_alpha=8, n_beta=64, b_list=[2, 32, 256], pipe_smax=3)
+    ctxs = [P.Context(0), P.Context(0)]
+    specs = [c.prepare(sw) for c in ctxs]
+    n = ctxs[0].sweep_size(specs[0])
+    ref, rnf = ctxs[0].topk(specs[0], 64)
+    for _ in range(20):
+        hits, nf = ctxs[0].topk(specs[0], 64)
+        assert hits == ref and nf == rnf
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs = [(torch.empty((64, 2), dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev))
+            for _ in range(2)]
+    for rep in range(5):
+        for c, sp, st, (h, cnt) in zip(ctxs, specs, streams, outs):
+            c.topk_async(sp, 0, n, 0, 1, 64, h.data_ptr(), cnt.data_ptr(), stream=st)
+        torch.cuda.synchronize()
+        for h, cnt in outs:
+            got = [int(v) % (1 << 64) for v in h.cpu().numpy()[:, 0]]
+            assert got == [x[0] for x in ref] and int(cnt.item()) == rnf
