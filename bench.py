@@ -62,10 +62,12 @@ def fp64_per_config(sb) -> float:
     fam = W.FAMILY_NAMES[sb.family]
     nab = max(1, len(sb.alpha)) * max(1, len(sb.beta))
     if fam == "pipeline" and sb.part_mode == W.PART_MASK and nab * max(1, len(sb.S)) * max(1, len(sb.dims)) == 1:
-        # one configuration per mask (cfg3-ii): every configuration is its own structure, so the
-        # whole canonical tree runs per configuration except its per-stage-count constants
-        # (cseg, pp_c): (cseg FB) tau, U tau, +, bS D(delta maxY), * beta, alpha +, pp_c *, comp + P, * I
-        return 10.0
+        # one configuration per mask (cfg3-ii): every configuration is its own structure. The
+        # canonical tree per mask, with what is invariant per stage count (cseg, pp_c, alpha,
+        # beta) and per table entry (U tau, bS D(delta Y) beta: a maximum of monotone products
+        # is the product of the maximum) hoisted exactly: D(maxF + maxB), x cseg, x tau,
+        # + U tau, alpha + Yb, x pp_c, comp + P2P, x I = 8 (DESIGN.md §5.1 mask blocks)
+        return 8.0
     if fam in ("pd", "pipeline") and nab < 32:
         n_s, n_d = max(1, len(sb.S)), max(1, len(sb.dims))
         g = 3.0 * math.ceil(n_s / 4) / n_s if fam == "pd" else 0.0
@@ -426,6 +428,7 @@ def ours(args):
         if os.path.exists(fp_path):
             try:
                 ncu_fp = json.load(open(fp_path)).get(sweep.name, {}).get(fam_name)
+                ncu_fp = float(ncu_fp) if ncu_fp is not None else None
             except Exception:
                 ncu_fp = None
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T fp64-pipe inst/s",

@@ -315,6 +315,7 @@ struct SubPlan {
     SubHdr hdr{};
     int family = 0, model = 0;   // model = ctx model id
     int64_t bmax = 0;            // largest batch value
+    bool dims0_pow2 = true;      // every dims[0] value a power of two
 };
 
 struct Plan {
@@ -348,6 +349,11 @@ static bool merge_level_off() {
 // (tile_body_blocked) instead of mode 3 (tile_body_comb); same results
 static bool comb_off() {
     static const bool off = getenv("PARADL_NO_COMB") != nullptr;
+    return off;
+}
+// A/B switch for experiments: PARADL_NO_MASKS=1 keeps screened mask blocks on the unsorted table
+static bool masks_off() {
+    static const bool off = getenv("PARADL_NO_MASKS") != nullptr;
     return off;
 }
 // A/B switch for experiments: PARADL_NO_STRUCT_TABLE=1 recomputes pipeline structure terms
@@ -436,6 +442,7 @@ static paradl_status plan_sweep_build(paradl_ctx *c, const paradl_sweep_spec *sp
                                     ? d[0]
                                     : 1;
             degmax = std::max(degmax, deg);
+            sp.dims0_pow2 = sp.dims0_pow2 && (d[0] & (d[0] - 1)) == 0;
             pmax = std::max<int64_t>(pmax, (int64_t)d[0] * d[1] * d[2] * d[3]);
         }
         std::vector<int32_t> Ll(s.Ls, s.Ls + s.n_Ls);
@@ -813,6 +820,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 if (mode == 3) {
                     w.cmb_off = a.memo_bytes;
                     a.memo_bytes += (uint32_t)align16(cmb_bytes);
+                    if (fam != PARADL_PD || P.subs[q].dims0_pow2) w.flags |= kWorkPow2;
                 }
                 if (mode == 1 && (fam == PARADL_PIPELINE || fam == PARADL_PD)) {
                     // screened path: per-lane dims table (ge_c, ge_s fp64 + ge_t u8) per thread
@@ -830,9 +838,13 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     if (hm.FB < lim && hm.WU < lim && memb < lim && (__int128)c->sys.delta * hm.Ymax < lim)
                         w.flags |= kWorkMaskD;
                 }
+                if (mode == 2 && (w.flags & kWorkMaskD) && fam == PARADL_PIPELINE && Q == 1 && h.radix[D_FLOPS] == 1 &&
+                    c->sys.n_tiers <= 4 && !masks_off())
+                    w.flags |= kWorkMaskS;
                 if (mode == 2) {
                     w.low_off = a.low_bytes / 64;
-                    a.low_bytes += h.radix[D_B] * 256u * 64u;
+                    // LowD (natural mask order) per b, then (kWorkMaskS) the sorted LowS table per b
+                    a.low_bytes += h.radix[D_B] * 256u * 64u * ((w.flags & kWorkMaskS) ? 2u : 1u);
                 }
             } else {
                 stride_digits(h, w);

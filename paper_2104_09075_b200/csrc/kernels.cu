@@ -33,6 +33,10 @@ namespace paradl {
 #ifndef PARADL_PIPE_MINB
 #define PARADL_PIPE_MINB PARADL_MINB
 #endif
+#ifndef PARADL_COMB_UNROLL
+#define PARADL_COMB_UNROLL 2
+#endif
+constexpr int kCombUnroll = PARADL_COMB_UNROLL;   // mode-3 p_d loop unroll (A/B knob)
 #ifndef PARADL_PIPE_KEYS
 #define PARADL_PIPE_KEYS 16
 #endif
@@ -2164,6 +2168,7 @@ __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64
 // the stage straddling bit 8 (from the last low cut to the first high cut) is formed.
 // All quantities are exact int64 sums / maxima, so the composition equals stage_terms.
 constexpr int kLowBits = 8;
+constexpr int kLowBitsMax = kLowBits;
 struct LowE {
     int64_t F, B, U, W, memI, maxY, sumY;
     int32_t e_last, pop;
@@ -2180,6 +2185,48 @@ struct __align__(16) LowD {
 struct __align__(16) NTab {
     double cseg, ppc, aw, bw;
 };
+// (kWorkMaskS) the low-bit table sorted by (e, pop) -- e = bit length of the low mask x (the row
+// after its last low cut), pop = popcount(x) -- with the per-configuration factors folded in:
+// Ut = U tau and Yb[t] = Ypp beta_t (P2P column of tier t).  Exact: max(a, b) x c = max(a c, b c)
+// and a + max(u, v) = max(a + u, a + v) for round-to-nearest and c > 0 (monotone), so
+// max(U, T_U) tau and pp_c (alpha + max(Ypp, hpps) beta) are maxima of precomputed parts.
+struct __align__(16) LowS {
+    double F, B, Ut, M;
+    double Yb[4];
+};
+static_assert(sizeof(LowS) == 64, "LowS layout");
+// start / size of the (e, pop) subgroups in the sorted table: e = 0 holds x = 0; e >= 1 holds
+// x in [2^(e-1), 2^e) ordered by pop (1..e), each subgroup C(e-1, pop-1) masks by x ascending
+struct SubTab {
+    uint16_t start[kLowBitsMax + 1][kLowBitsMax + 2], cnt[kLowBitsMax + 1][kLowBitsMax + 2];
+};
+constexpr SubTab make_subtab() {
+    SubTab t{};
+    for (int e = 0; e <= kLowBitsMax; e++) {
+        int start = e ? 1 << (e - 1) : 0;
+        for (int pop = 0; pop <= kLowBitsMax + 1; pop++) {
+            int c = 0;
+            if (e == 0) c = pop == 0 ? 1 : 0;
+            else if (pop >= 1 && pop <= e) {   // C(e-1, pop-1)
+                long long v = 1;
+                for (int j = 0; j < pop - 1; j++) v = v * (e - 1 - j) / (j + 1);
+                c = (int)v;
+            }
+            t.start[e][pop] = (uint16_t)start;
+            t.cnt[e][pop] = (uint16_t)c;
+            start += c;
+        }
+    }
+    return t;
+}
+__constant__ SubTab kSub = make_subtab();
+// sorted position of low mask x
+__device__ __forceinline__ int lows_pos(uint32_t x) {
+    const int e = x ? 32 - __clz(x) : 0, pop = __popc(x);
+    int r = 0;   // rank of x among the masks of its (e, pop) subgroup
+    for (uint32_t y = e ? 1u << (e - 1) : 0u; y < x; y++) r += __popc(y) == pop;
+    return kSub.start[e][pop] + r;
+}
 static_assert(sizeof(LowD) == 64, "LowD layout");
 
 // Largest integer m with gamma (delta m) <= cap (Table 2 mem row), -1 if none:
@@ -2291,6 +2338,42 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
             const NTab *nt = reinterpret_cast<const NTab *>(C.memo + (size_t)nb * (C.nS + C.nD)) +
                              (size_t)L.d[D_B] * kMaskTabN;
             const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
+            if (w.flags & kWorkMaskS) {
+                // sorted table: per (e, pop) subgroup the stage count, its tier and NTab row and the
+                // high part's P2P term are fixed; per mask 8 fp64 operations of the canonical tree
+                // (FB, cseg FB, x tau, + U tau; alpha + Yb, x pp_c; comp + P2P, x I) and the maxima
+                const LowS *lsb = reinterpret_cast<const LowS *>(lowtab + (size_t)nb * 256u) + (size_t)L.d[D_B] * 256u;
+                for (int e = 0; e <= kLowBits; e++) {
+                    const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
+                    const double TUt = dmul(fmax(i2d(cU - PU[e]), hUd), tau);
+                    const double TM = fmax(i2d(2 * b * (cX - PX[e]) + 2 * (cW - PW[e]) + (cI - PI[e])), hMd);
+                    const bool grp_ok = seg_ok && TM <= mem_max_d;
+                    for (int pop = e ? 1 : 0; pop <= e; pop++) {
+                        const int ns = pop + hpop + 1;
+                        const NTab tq = nt[ns];
+                        const int tr = tier_by_n[ns];
+                        const bool ok = grp_ok && tr >= 0;
+                        const int tt = max(tr, 0);
+                        const double Ph = dmul(tq.ppc, dadd(tq.aw, dmul(hpps, tq.bw)));
+                        const int j0 = kSub.start[e][pop], j1 = j0 + kSub.cnt[e][pop];
+#pragma unroll 2
+                        for (int j = j0; j < j1; j++) {
+                            const double2 *qp = reinterpret_cast<const double2 *>(lsb + j);
+                            const double2 qFB = qp[0], qUM = qp[1];
+                            const double yb = lsb[j].Yb[tt];
+                            const double maxF = qFB.x > TF ? qFB.x : TF, maxB = qFB.y > TB ? qFB.y : TB;
+                            const double mUt = qUM.x > TUt ? qUM.x : TUt;
+                            const double Pl = dmul(tq.ppc, dadd(tq.aw, yb));
+                            const double p2p = Pl > Ph ? Pl : Ph;
+                            const double comp = dadd(dmul(dmul(tq.cseg, dadd(maxF, maxB)), tau), mUt);
+                            const double key = dmul(dadd(comp, p2p), I);
+                            const bool feas = ok & (qUM.y <= mem_max_d);
+                            nok += feas ? 1u : 0u;
+                            hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
+                        }
+                    }
+                }
+            } else
             for (int e = 0; e <= kLowBits; e++) {
                 const int x0 = e ? 1 << (e - 1) : 0, x1 = e ? 1 << e : 1;
                 const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
@@ -2661,12 +2744,11 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 P[u][2] = dmul(q.ppc, dadd(at1, x0));
                 P[u][3] = dmul(q.ppc, dadd(at1, x1));
             }
-#pragma unroll 1
-            for (uint32_t iD = 0; iD < nD; iD++) {
-                const CmbD d = drow[iD];
+            // per p_d value: the GE terms G = ge_c (alpha + ge_s beta) of the 2 x 2 rows, then the
+            // 16 keys t = comp + G, t = t + P, key = t I and their smallest high word
+            auto dims_keys = [&](const CmbD &d, double gs) {
                 double Gq[4] = {0.0, 0.0, 0.0, 0.0};
                 if (FAM == PARADL_PD) {
-                    const double gs = d.div ? ddiv_rare(mW, i2d(d.pd)) : dmul(mW, d.scale);
                     const double g0 = dmul(gs, d.b0), g1 = dmul(gs, d.b1);
                     Gq[0] = dmul(d.gc, dadd(d.a0, g0));
                     Gq[1] = dmul(d.gc, dadd(d.a0, g1));
@@ -2682,6 +2764,19 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                         h[q] = __double2hiint(dmul(t, d.I));
                     }
                     hmin = min(hmin, min(min(h[0], h[1]), min(h[2], h[3])));
+                }
+            };
+            if (w.flags & kWorkPow2) {   // every p_d a power of two: ge_s = mW 2^-k, no branch
+#pragma unroll kCombUnroll
+                for (uint32_t iD = 0; iD < nD; iD++) {
+                    const CmbD d = drow[iD];
+                    dims_keys(d, dmul(mW, d.scale));
+                }
+            } else {
+#pragma unroll 1
+                for (uint32_t iD = 0; iD < nD; iD++) {
+                    const CmbD d = drow[iD];
+                    dims_keys(d, d.div ? ddiv_rare(mW, i2d(d.pd)) : dmul(mW, d.scale));
                 }
             }
         }
@@ -2924,6 +3019,21 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                     d.Ypp = dmul(ddiv(i2d(b), i2d(Sv[0])), dmul(i2d(v.H->delta), d.Y));
                     d.pad_ = 0.0;
                     reinterpret_cast<LowD *>(low_base + w.low_off)[e] = d;
+                    if (w.flags & kWorkMaskS) {
+                        // sorted copy with tau and the P2P betas folded in (one flops value, one
+                        // beta row: the host checked Q == 1 and radix[D_FLOPS] == 1)
+                        const double tau = ddiv(1.0, at<double>(v.img, S->off_flops)[0]);
+                        const double *be = at<double>(v.img, S->off_beta);
+                        LowS q;
+                        q.F = d.F;
+                        q.B = d.B;
+                        q.Ut = dmul(d.U, tau);
+                        q.M = d.M;
+                        for (int t = 0; t < 4; t++)
+                            q.Yb[t] = t < v.H->n_ctiers ? dmul(d.Ypp, be[t + v.H->p2p_off]) : 0.0;
+                        LowS *ls = reinterpret_cast<LowS *>(low_base + w.low_off + S->radix[D_B] * 256u);
+                        ls[(size_t)ib * 256u + lows_pos(x)] = q;
+                    }
                 } else {
                     (low_base + w.low_off)[e] = L;
                 }

@@ -23,6 +23,9 @@ constexpr int kMaxModelsPerSweep = 8;
 constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kWorkMaskD = 1u;
+constexpr uint32_t kWorkPow2 = 2u;       // mode 3: every dims p_d is a power of two (ge_s by an exact scale)
+constexpr uint32_t kWorkMaskS = 4u;      // mode 2 (kWorkMaskD, one configuration per mask, one flops value):
+                                         // the screen reads the (e, pop)-sorted table with tau / beta folded in
 constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the screened mask path (n <= 64)
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
