@@ -784,7 +784,19 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             h.radix[D_BETA] <= 2 && cmb_bytes <= (32u << 10) && !comb_off() &&
             smem + kLaneStateBytes + cmb_bytes + memo_n * sizeof(double) + 1024 <= c->smem_optin)
             mode = 3;
-        const uint64_t unit = mode == 2 ? Q << 8 : Q;
+        // screened masks hold every stage quantity as an exact double: the model totals bound
+        // each stage term, so they must stay below 2^53 (kWorkMaskD)
+        bool maskd_ok = false;
+        if (mode == 2 && maskd_n) {
+            const HostModel &hm = c->models[P.subs[q].model];
+            const __int128 lim = (__int128)1 << 53;
+            const __int128 memb = 2 * (__int128)P.subs[q].bmax * hm.XY + 2 * hm.W + hm.BI;
+            maskd_ok = hm.FB < lim && hm.WU < lim && memb < lim && (__int128)c->sys.delta * hm.Ymax < lim;
+        }
+        // sorted 512-mask blocks (kWorkMaskS, tile_body_mask_s): one flops value, <= 4 tiers
+        const bool masks_ok = maskd_ok && h.radix[D_FLOPS] == 1 && c->sys.n_tiers <= 4 && !masks_off();
+        const int low_bits = masks_ok ? kLowBitsSorted : 8;
+        const uint64_t unit = mode == 2 ? Q << low_bits : Q;
         const uint64_t lo = r0 - s0, hi = r1 - s0;
         uint64_t b0 = lo, b1 = lo;   // [b0, b1): blocked part
         if (mode) {
@@ -812,7 +824,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             if (pi == 1) {
                 w.mode = mode;
                 memset(w.inc, 0, sizeof w.inc);
-                w.inc_part = mode == 2 ? 256 : 1;
+                w.inc_part = mode == 2 ? (1ull << low_bits) : 1;
                 w.inc_top = D_PART;
                 w.memo_n = (uint32_t)memo_n;
                 w.memo_off = a.memo_bytes;
@@ -828,23 +840,13 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     const uint32_t tb = (uint32_t)align16((size_t)nD * 8u * kThreads);
                     if (tb <= kMaxDtabBytes) a.dtab_bytes = std::max(a.dtab_bytes, tb);
                 }
-                if (mode == 2 && maskd_n) {
-                    // screened mask blocks hold every stage quantity as an exact double: the
-                    // model totals bound each stage term, so they must stay below 2^53
-                    const HostModel &hm = c->models[P.subs[q].model];
-                    const int64_t bmax = P.subs[q].bmax;
-                    const __int128 lim = (__int128)1 << 53;
-                    const __int128 memb = 2 * (__int128)bmax * hm.XY + 2 * hm.W + hm.BI;
-                    if (hm.FB < lim && hm.WU < lim && memb < lim && (__int128)c->sys.delta * hm.Ymax < lim)
-                        w.flags |= kWorkMaskD;
-                }
-                if (mode == 2 && (w.flags & kWorkMaskD) && fam == PARADL_PIPELINE && Q == 1 && h.radix[D_FLOPS] == 1 &&
-                    c->sys.n_tiers <= 4 && !masks_off())
-                    w.flags |= kWorkMaskS;
+                if (maskd_ok) w.flags |= kWorkMaskD;
+                if (masks_ok) w.flags |= kWorkMaskS;
                 if (mode == 2) {
                     w.low_off = a.low_bytes / 64;
-                    // LowD (natural mask order) per b, then (kWorkMaskS) the sorted LowS table per b
-                    a.low_bytes += h.radix[D_B] * 256u * 64u * ((w.flags & kWorkMaskS) ? 2u : 1u);
+                    // 64-byte entries per b: LowE / LowD over 256 low masks, or (kWorkMaskS) the
+                    // sorted LowS table over 512
+                    a.low_bytes += h.radix[D_B] * (1u << low_bits) * 64u;
                 }
             } else {
                 stride_digits(h, w);
@@ -998,7 +1000,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const SubHdr &h = P.subs[w.sub].hdr;
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
-                const uint64_t nblk = range / (w.mode == 2 ? Q << 8 : Q);
+                const uint64_t nblk = range / (w.mode == 2 ? Q << ((w.flags & kWorkMaskS) ? kLowBitsSorted : 8) : Q);
                 // >= ~16 tiles per warp of this rank's shard (the last wave of a dynamic tile queue
                 // leaves at most one tile per warp unbalanced: <= ~6 % at 8 shards of cfg5);
                 // 1..256 partitions per lane per tile

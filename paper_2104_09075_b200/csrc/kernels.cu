@@ -2168,7 +2168,8 @@ __device__ void tile_body_blocked(const LaunchArgs &a, const WorkItem &w, uint64
 // the stage straddling bit 8 (from the last low cut to the first high cut) is formed.
 // All quantities are exact int64 sums / maxima, so the composition equals stage_terms.
 constexpr int kLowBits = 8;
-constexpr int kLowBitsMax = kLowBits;
+constexpr int kLowBitsS = kLowBitsSorted;    // sorted mask path (kWorkMaskS): 512-mask blocks
+constexpr int kLowBitsMax = kLowBitsS;
 struct LowE {
     int64_t F, B, U, W, memI, maxY, sumY;
     int32_t e_last, pop;
@@ -2338,42 +2339,6 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
             const NTab *nt = reinterpret_cast<const NTab *>(C.memo + (size_t)nb * (C.nS + C.nD)) +
                              (size_t)L.d[D_B] * kMaskTabN;
             const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
-            if (w.flags & kWorkMaskS) {
-                // sorted table: per (e, pop) subgroup the stage count, its tier and NTab row and the
-                // high part's P2P term are fixed; per mask 8 fp64 operations of the canonical tree
-                // (FB, cseg FB, x tau, + U tau; alpha + Yb, x pp_c; comp + P2P, x I) and the maxima
-                const LowS *lsb = reinterpret_cast<const LowS *>(lowtab + (size_t)nb * 256u) + (size_t)L.d[D_B] * 256u;
-                for (int e = 0; e <= kLowBits; e++) {
-                    const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
-                    const double TUt = dmul(fmax(i2d(cU - PU[e]), hUd), tau);
-                    const double TM = fmax(i2d(2 * b * (cX - PX[e]) + 2 * (cW - PW[e]) + (cI - PI[e])), hMd);
-                    const bool grp_ok = seg_ok && TM <= mem_max_d;
-                    for (int pop = e ? 1 : 0; pop <= e; pop++) {
-                        const int ns = pop + hpop + 1;
-                        const NTab tq = nt[ns];
-                        const int tr = tier_by_n[ns];
-                        const bool ok = grp_ok && tr >= 0;
-                        const int tt = max(tr, 0);
-                        const double Ph = dmul(tq.ppc, dadd(tq.aw, dmul(hpps, tq.bw)));
-                        const int j0 = kSub.start[e][pop], j1 = j0 + kSub.cnt[e][pop];
-#pragma unroll 2
-                        for (int j = j0; j < j1; j++) {
-                            const double2 *qp = reinterpret_cast<const double2 *>(lsb + j);
-                            const double2 qFB = qp[0], qUM = qp[1];
-                            const double yb = lsb[j].Yb[tt];
-                            const double maxF = qFB.x > TF ? qFB.x : TF, maxB = qFB.y > TB ? qFB.y : TB;
-                            const double mUt = qUM.x > TUt ? qUM.x : TUt;
-                            const double Pl = dmul(tq.ppc, dadd(tq.aw, yb));
-                            const double p2p = Pl > Ph ? Pl : Ph;
-                            const double comp = dadd(dmul(dmul(tq.cseg, dadd(maxF, maxB)), tau), mUt);
-                            const double key = dmul(dadd(comp, p2p), I);
-                            const bool feas = ok & (qUM.y <= mem_max_d);
-                            nok += feas ? 1u : 0u;
-                            hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
-                        }
-                    }
-                }
-            } else
             for (int e = 0; e <= kLowBits; e++) {
                 const int x0 = e ? 1 << (e - 1) : 0, x1 = e ? 1 << e : 1;
                 const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
@@ -2425,6 +2390,164 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
         }
         tk.refresh();
         if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 256
+    }
+}
+
+// Mode 2, sorted (kWorkMaskS: pipeline masks, one configuration per mask, one flops value, the
+// cfg3-ii shape).  Lanes own blocks of 2^kLowBitsS = 512 masks; the only per-CTA table is the
+// (e, pop)-sorted LowS (U tau and Ypp beta_t folded in, §5.1).  Per (e, pop) subgroup the stage
+// count, its tier and NTab row and the high part's P2P term are registers; per mask 8 fp64
+// operations and 5 compares.  A block whose screen passes (0.2 % of the work in cfg3-ii) forms
+// each mask's low stage terms from the prefix sums and re-evaluates it through eval_partition.
+template <int FAM>
+__device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
+                                 uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
+                                 const LowS *lows, const int8_t *tier_by_n) {
+    constexpr int LB = kLowBitsS;
+    BlkCtx C = make_blk(w, smem, memo);
+    const View &v = C.v;
+    const ModelHdr *M = v.M;
+    const ImgHdr *H = v.H;
+    const int lane = threadIdx.x & 31;
+    const int G = M->G;
+    const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+    const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+    const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+    const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+    const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+    const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+    const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+    const uint64_t span = C.Q << LB;   // Q == 1
+    const uint64_t nblk = (w.hi - w.lo) / span;
+    const uint64_t c = w.steps;
+    const uint64_t blk0 = (tile * 32 + lane) * c;
+    const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
+    const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)nmine);
+    const double dd = i2d(H->delta);
+    const int64_t Sg = C.Sv[0];
+    const uint32_t nb = v.S->radix[D_B];
+    double cap_memo = CUDART_NAN, mem_max_d = -1.0;
+    Lane L;
+    if (nmine) decode(v, w.lo + blk0 * span, L, cuts, kThreads);
+    for (uint32_t it = 0; it < iters; it++) {
+        const bool act = it < nmine;
+        const uint64_t hi_mask = L.part & ~(((uint64_t)1 << LB) - 1);
+        int64_t hF = 0, hB = 0, hU = 0, hM = 0, hY = 0;
+        int c_h = G;
+        int hpop = 0;
+        int64_t b = 1;
+        int hmin = 0x7fffffff;
+        uint32_t nok = 0;
+        if (act) {
+            b = at<int64_t>(v.img, v.S->off_b)[L.d[D_B]];
+            uint64_t m = hi_mask;
+            hpop = __popcll(m);
+            if (m) {   // stages after the first high cut (exact int64)
+                c_h = __ffsll((long long)m);
+                m &= m - 1;
+                int beg = c_h;
+                hY = Y[c_h - 1];
+                for (;;) {
+                    const int end = m ? __ffsll((long long)m) : G;
+                    m &= m - 1;
+                    hF = max(hF, PF[end] - PF[beg]);
+                    hB = max(hB, PB[end] - PB[beg]);
+                    hU = max(hU, PU[end] - PU[beg]);
+                    hM = max(hM, 2 * b * (PX[end] - PX[beg]) + 2 * (PW[end] - PW[beg]) + (PI[end] - PI[beg]));
+                    if (end == G) break;
+                    hY = max(hY, Y[end - 1]);
+                    beg = end;
+                }
+            }
+            const double cap = at<double>(v.img, v.S->off_cap)[L.d[D_CAP]];
+            const double R = at<double>(v.img, v.S->off_flops)[L.d[D_FLOPS]];
+            if (R != C.R_memo) {
+                C.R_memo = R;
+                C.tau = ddiv(1.0, R);
+            }
+            if (!(cap == cap_memo)) {
+                cap_memo = cap;
+                mem_max_d = i2d(mem_threshold(H, cap));
+            }
+            const double tau = C.tau;
+            const double *mrow = C.memo + (size_t)L.d[D_B] * (C.nS + C.nD);
+            const double bS = mrow[0], I = mrow[C.nS];
+            const bool seg_ok = Sg >= 1 && Sg <= b;
+            const double hFd = i2d(hF), hBd = i2d(hB), hUd = i2d(hU), hMd = i2d(hM);
+            const double hpps = dmul(bS, dmul(dd, i2d(hY)));
+            const NTab *nt = reinterpret_cast<const NTab *>(C.memo + (size_t)nb * (C.nS + C.nD)) +
+                             (size_t)L.d[D_B] * kMaskTabN;
+            const LowS *lsb = lows + ((size_t)L.d[D_B] << LB);
+            const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
+            for (int e = 0; e <= LB; e++) {
+                // straddling stage (e, c_h] folded with the high stages
+                const double TF = fmax(i2d(cF - PF[e]), hFd), TB = fmax(i2d(cB - PB[e]), hBd);
+                const double TUt = dmul(fmax(i2d(cU - PU[e]), hUd), tau);
+                const double TM = fmax(i2d(2 * b * (cX - PX[e]) + 2 * (cW - PW[e]) + (cI - PI[e])), hMd);
+                const bool grp_ok = seg_ok && TM <= mem_max_d;   // memI = max(low, T) <= mem_max <=> both
+                for (int pop = e ? 1 : 0; pop <= e; pop++) {
+                    const int ns = pop + hpop + 1;
+                    const NTab tq = nt[ns];
+                    const int tr = tier_by_n[ns];
+                    const bool ok = grp_ok && tr >= 0;
+                    const int tt = max(tr, 0);
+                    const double Ph = dmul(tq.ppc, dadd(tq.aw, dmul(hpps, tq.bw)));
+                    const int j0 = kSub.start[e][pop], j1 = j0 + kSub.cnt[e][pop];
+#pragma unroll 2
+                    for (int j = j0; j < j1; j++) {
+                        const double2 *qp = reinterpret_cast<const double2 *>(lsb + j);
+                        const double2 qFB = qp[0], qUM = qp[1];
+                        const double yb = lsb[j].Yb[tt];
+                        const double maxF = qFB.x > TF ? qFB.x : TF, maxB = qFB.y > TB ? qFB.y : TB;
+                        const double mUt = qUM.x > TUt ? qUM.x : TUt;
+                        const double Pl = dmul(tq.ppc, dadd(tq.aw, yb));
+                        const double p2p = Pl > Ph ? Pl : Ph;
+                        const double comp = dadd(dmul(dmul(tq.cseg, dadd(maxF, maxB)), tau), mUt);
+                        const double key = dmul(dadd(comp, p2p), I);
+                        const bool feas = ok & (qUM.y <= mem_max_d);
+                        nok += feas ? 1u : 0u;
+                        hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
+                    }
+                }
+            }
+        }
+        cnt += nok;
+        const bool maybe = act && hmin <= __double2hiint(tk.adm);
+        if (__any_sync(0xffffffffu, maybe)) {
+            const uint64_t gbase = v.S->offset + w.lo + (blk0 + it) * span;
+            for (uint32_t x = 0; x < (1u << LB); x++) {
+                StageT st;
+                int64_t ns = 1;
+                if (maybe) {
+                    // low stages of mask x (cuts among the first LB + 1 rows), then the straddling
+                    // stage (e_last, c_h] and the high maxima: exact int64, = stage_terms
+                    int64_t lF = 0, lB = 0, lU = 0, lM = 0, lY = 0;
+                    int beg = 0;
+                    uint32_t mm = x;
+                    while (mm) {
+                        const int end = __ffs(mm);
+                        mm &= mm - 1;
+                        lF = max(lF, PF[end] - PF[beg]);
+                        lB = max(lB, PB[end] - PB[beg]);
+                        lU = max(lU, PU[end] - PU[beg]);
+                        lM = max(lM, 2 * b * (PX[end] - PX[beg]) + 2 * (PW[end] - PW[beg]) + (PI[end] - PI[beg]));
+                        lY = max(lY, Y[end - 1]);
+                        beg = end;
+                    }
+                    st.maxF = max(max(lF, PF[c_h] - PF[beg]), hF);
+                    st.maxB = max(max(lB, PB[c_h] - PB[beg]), hB);
+                    st.maxU = max(max(lU, PU[c_h] - PU[beg]), hU);
+                    st.maxW = 0;   // pd only
+                    st.sumY = 0;   // layer-pure only
+                    st.memI = max(max(lM, 2 * b * (PX[c_h] - PX[beg]) + 2 * (PW[c_h] - PW[beg]) + (PI[c_h] - PI[beg])), hM);
+                    st.maxY = max(lY, hY);
+                    ns = __popc(x) + hpop + 1;
+                }
+                eval_partition<FAM, false>(C, maybe, L, st, ns, gbase + (uint64_t)x * C.Q, tk, cnt);
+            }
+        }
+        tk.refresh();
+        if (it + 1 < nmine) advance(w, v, L, cuts, kThreads);   // next block: inc_part = 512
     }
 }
 
@@ -2976,7 +3099,46 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 tab[e] = ddiv(i2d(v.M->D), i2d(b * pd));
             }
         }
-        if (w.mode == 2) {
+        if (w.mode == 2 && (w.flags & kWorkMaskS)) {
+            // the (e, pop)-sorted table of 2^kLowBitsS low masks per b, tau / P2P betas folded in
+            const ModelHdr *M = v.M;
+            const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
+            const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
+            const int64_t *PU = at<int64_t>(v.mb, M->off_pu);
+            const int64_t *PW = at<int64_t>(v.mb, M->off_pw);
+            const int64_t *PX = at<int64_t>(v.mb, M->off_pxy);
+            const int64_t *PI = at<int64_t>(v.mb, M->off_pbi);
+            const int64_t *Y = at<int64_t>(v.mb, M->off_y);
+            const double tau = ddiv(1.0, at<double>(v.img, S->off_flops)[0]);
+            const double *be = at<double>(v.img, S->off_beta);
+            LowS *ls = reinterpret_cast<LowS *>(low_base + w.low_off);
+            const uint32_t n = S->radix[D_B] << kLowBitsS;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+                const uint32_t ib = e >> kLowBitsS, x = e & ((1u << kLowBitsS) - 1);
+                const int64_t b = bv[ib];
+                int64_t F = 0, B = 0, U = 0, Mm = 0, Yy = 0;
+                int beg = 0;
+                uint32_t m = x;
+                while (m) {   // stages [beg, end) closed by low cuts
+                    const int end = __ffs(m);
+                    m &= m - 1;
+                    F = max(F, PF[end] - PF[beg]);
+                    B = max(B, PB[end] - PB[beg]);
+                    U = max(U, PU[end] - PU[beg]);
+                    Mm = max(Mm, 2 * b * (PX[end] - PX[beg]) + 2 * (PW[end] - PW[beg]) + (PI[end] - PI[beg]));
+                    Yy = max(Yy, Y[end - 1]);
+                    beg = end;
+                }
+                const double Ypp = dmul(ddiv(i2d(b), i2d(Sv[0])), dmul(i2d(v.H->delta), i2d(Yy)));
+                LowS q;
+                q.F = i2d(F);
+                q.B = i2d(B);
+                q.Ut = dmul(i2d(U), tau);
+                q.M = i2d(Mm);
+                for (int t = 0; t < 4; t++) q.Yb[t] = t < v.H->n_ctiers ? dmul(Ypp, be[t + v.H->p2p_off]) : 0.0;
+                ls[((size_t)ib << kLowBitsS) + lows_pos(x)] = q;
+            }
+        } else if (w.mode == 2) {
             const ModelHdr *M = v.M;
             const int64_t *PF = at<int64_t>(v.mb, M->off_pf);
             const int64_t *PB = at<int64_t>(v.mb, M->off_pb);
@@ -3019,21 +3181,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                     d.Ypp = dmul(ddiv(i2d(b), i2d(Sv[0])), dmul(i2d(v.H->delta), d.Y));
                     d.pad_ = 0.0;
                     reinterpret_cast<LowD *>(low_base + w.low_off)[e] = d;
-                    if (w.flags & kWorkMaskS) {
-                        // sorted copy with tau and the P2P betas folded in (one flops value, one
-                        // beta row: the host checked Q == 1 and radix[D_FLOPS] == 1)
-                        const double tau = ddiv(1.0, at<double>(v.img, S->off_flops)[0]);
-                        const double *be = at<double>(v.img, S->off_beta);
-                        LowS q;
-                        q.F = d.F;
-                        q.B = d.B;
-                        q.Ut = dmul(d.U, tau);
-                        q.M = d.M;
-                        for (int t = 0; t < 4; t++)
-                            q.Yb[t] = t < v.H->n_ctiers ? dmul(d.Ypp, be[t + v.H->p2p_off]) : 0.0;
-                        LowS *ls = reinterpret_cast<LowS *>(low_base + w.low_off + S->radix[D_B] * 256u);
-                        ls[(size_t)ib * 256u + lows_pos(x)] = q;
-                    }
+
                 } else {
                     (low_base + w.low_off)[e] = L;
                 }
@@ -3084,7 +3232,10 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
                                     reinterpret_cast<int64_t *>(dtab));
         }
         else if (BLK == 2) {
-            if (FAM == PARADL_PIPELINE && (w.flags & kWorkMaskD))
+            if (FAM == PARADL_PIPELINE && (w.flags & kWorkMaskS))
+                tile_body_mask_s<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
+                                      reinterpret_cast<const LowS *>(lowtab + w.low_off), ex->tier_by_n);
+            else if (FAM == PARADL_PIPELINE && (w.flags & kWorkMaskD))
                 tile_body_mask_d<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
                                       reinterpret_cast<const LowD *>(lowtab + w.low_off), ex->tier_by_n);
             else

@@ -24,6 +24,7 @@ constexpr int kThreads = 256;            // threads per CTA of the sweep kernels
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kWorkMaskD = 1u;
 constexpr uint32_t kWorkPow2 = 2u;       // mode 3: every dims p_d is a power of two (ge_s by an exact scale)
+constexpr int kLowBitsSorted = 9;       // kWorkMaskS blocks: 2^9 masks (kernels.cu kLowBitsS)
 constexpr uint32_t kWorkMaskS = 4u;      // mode 2 (kWorkMaskD, one configuration per mask, one flops value):
                                          // the screen reads the (e, pop)-sorted table with tau / beta folded in
 constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the screened mask path (n <= 64)

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("cfg", type=int)
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--chunk-log2", type=int, default=30)
+    ap.add_argument("--stride", type=int, default=1,
+                    help="evaluate every stride-th chunk only (sampled chunks; no whole-sweep merge)")
     args = ap.parse_args()
 
     from oracle import oracle as O
@@ -49,7 +51,7 @@ def main():
             r = json.loads(ln)
             if r["n"] == n and r["chunk"] == chunk:
                 done[r["first"]] = r
-    firsts = list(range(0, n, chunk))
+    firsts = list(range(0, n, chunk))[::args.stride]
     t_all = time.time()
     with open(part, "a") as f:
         for a in firsts:
@@ -65,6 +67,9 @@ def main():
             f.flush()
             done[a] = r
             print(f"cfg{args.cfg} chunk {len(done)}/{len(firsts)} [{a}, +{c}) {r['seconds']:.1f} s", flush=True)
+    if args.stride > 1:
+        print(f"sampled chunks done: {len(done)} (every {args.stride}-th of {len(range(0, n, chunk))})")
+        return
     cand = []
     for r in done.values():
         cand += [(float.fromhex(k), i) for i, k in r["hits"]]
