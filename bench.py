@@ -230,6 +230,14 @@ def cpu_oracle_baseline(sweep, target_s: float, rank: int = 0):
                       f"({tot} configs, {dt:.1f} s, top-{K_TOP} + count per window)"}
 
 
+def bench_config(sweep, n_configs: int, ws: int) -> dict:
+    """The `config` object of both arms (same keys and values for the same workload)."""
+    return {"workload": sweep.name, "configs_per_step": int(n_configs), "k": K_TOP,
+            "model": "+".join(m.name for m in sweep.models) + " layer tables (paper Table 4 shapes)",
+            "parallelism": f"index-range shards x{ws} + NCCL all_gather merge",
+            "l2": "flushed (256 MiB device write) before every timed step; inputs are a KB-size image"}
+
+
 def reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
@@ -239,11 +247,12 @@ def reference_arm(args):
     base = {"metric": METRIC if args.scaling == "strong" or args.gpus <= 1 else METRIC_WEAK,
             "unit": "configs/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": sweep.name}}
+            "config": None}
     per_step_s = max(0.3, min(5.0, 120.0 / max(1, args.steps + args.warmup)))
     from oracle import oracle as O
     osw = O.OracleSweep(sweep)
     n = osw.size()
+    base["config"] = bench_config(sweep, n, dist_env()[0])
     cores = os.cpu_count() or 1
     # calibrate windows per step so one step takes about per_step_s seconds
     t0 = time.perf_counter()
@@ -533,10 +542,7 @@ def ours(args):
             "value": value, "unit": "configs/s", "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": sweep.name, "configs_per_step": N, "k": K_TOP,
-                       "model": "+".join(m.name for m in sweep.models) + " layer tables (paper Table 4 shapes)",
-                       "parallelism": f"index-range shards x{ws} + NCCL all_gather merge",
-                       "l2": "flushed (256 MiB device write) before every timed step; inputs are a KB-size image"},
+            "config": bench_config(sweep, N, ws),
             "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(gpu_launches),

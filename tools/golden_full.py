@@ -35,6 +35,12 @@ def main():
     ap.add_argument("--chunk-log2", type=int, default=30)
     ap.add_argument("--stride", type=int, default=1,
                     help="evaluate every stride-th chunk only (sampled chunks; no whole-sweep merge)")
+    ap.add_argument("--reverse", action="store_true", help="evaluate the chunks from the last one down")
+    ap.add_argument("--time-budget", type=float, default=0.0, help="stop starting chunks after this many seconds")
+    ap.add_argument("--out", default="", help="checkpoint file (default tests/golden/full_cfgN.partial.jsonl)")
+    ap.add_argument("--merge-only", action="store_true",
+                    help="no evaluation: merge every tests/golden/full_cfgN*.jsonl checkpoint (deduplicated by "
+                         "chunk) into full_cfgN.chunks.jsonl, and into full_cfgN.json when every chunk is there")
     args = ap.parse_args()
 
     from oracle import oracle as O
@@ -44,19 +50,33 @@ def main():
     n = osw.size()
     chunk = 1 << args.chunk_log2
     gdir = os.path.join(ROOT, "tests", "golden")
-    part = os.path.join(gdir, f"full_cfg{args.cfg}.partial.jsonl")
+    part = args.out or os.path.join(gdir, f"full_cfg{args.cfg}.partial.jsonl")
     done = {}
-    if os.path.exists(part):
-        for ln in open(part):
+    import glob
+    for path in sorted(set(glob.glob(os.path.join(gdir, f"full_cfg{args.cfg}*.jsonl")) + [part])):
+        if not os.path.exists(path):
+            continue
+        for ln in open(path):
             r = json.loads(ln)
             if r["n"] == n and r["chunk"] == chunk:
                 done[r["first"]] = r
     firsts = list(range(0, n, chunk))[::args.stride]
+    if args.reverse:
+        firsts = firsts[::-1]
     t_all = time.time()
+    if args.merge_only:
+        with open(os.path.join(gdir, f"full_cfg{args.cfg}.chunks.jsonl"), "w") as f:
+            for a in sorted(done):
+                f.write(json.dumps(done[a]) + "\n")
+        print(f"merged {len(done)} of {len(firsts)} chunks")
+        if len(done) < len(firsts):
+            return
     with open(part, "a") as f:
         for a in firsts:
             if a in done:
                 continue
+            if args.time_budget and time.time() - t_all > args.time_budget:
+                break
             c = min(chunk, n - a)
             t0 = time.time()
             hits, nf = osw.topk(a, c, K, nthreads=args.threads)
@@ -69,6 +89,9 @@ def main():
             print(f"cfg{args.cfg} chunk {len(done)}/{len(firsts)} [{a}, +{c}) {r['seconds']:.1f} s", flush=True)
     if args.stride > 1:
         print(f"sampled chunks done: {len(done)} (every {args.stride}-th of {len(range(0, n, chunk))})")
+        return
+    if len(done) < len(firsts):
+        print(f"{len(done)} of {len(firsts)} chunks done; no whole-sweep file yet")
         return
     cand = []
     for r in done.values():
