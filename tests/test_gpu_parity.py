@@ -730,3 +730,44 @@ def test_repeated_and_concurrent_calls_identical(dev):
         for h, cnt in outs:
             got = [int(v) % (1 << 64) for v in h.cpu().numpy()[:, 0]]
             assert got == [x[0] for x in ref] and int(cnt.item()) == rnf
+
+
+def test_calibrated_system_sweep_vs_oracle(dev, oracle_mod):
+    """f2: a system assembled by workloads.calibrate from fitted parameters --
+    ring-form tiers per group size, the tree form and its crossing as tree_threshold_B, the
+    point-to-point fit as p2p scales (Q40), measured per-layer times as the layer table -- swept
+    on the GPU (cfg2 shape, cfg5 shape) against the oracle.  The timings are synthetic Hockney
+    samples with noise (the fits and the gloo measurement path are tested on CPU)."""
+    from workloads import calibrate as CAL
+    from workloads import models as M
+    rng = random.Random(3)
+    sizes = [1 << e for e in range(10, 29, 2)]
+    tiers = []
+    for p, (a, b) in ((2, (15e-6, 1 / 490e9)), (4, (6e-6, 1 / 580e9)), (1024, (4e-5, 1 / 25e9))):
+        t = [2 * (p - 1) * (a + m / p * b) * (1 + rng.uniform(-0.03, 0.03)) for m in sizes]
+        fa, fb, _ = CAL.fit_allreduce(p, sizes, t)
+        tiers.append({"p": p, "alpha_s": fa, "beta_s_per_B": fb})
+    lg = 2
+    tt = [2 * (lg + 2) * (3e-6 + m / 4 * (1 / 90e9)) for m in sizes]
+    tree = CAL.fit_allreduce_tree(4, sizes, tt, 2)
+    thr = CAL.tree_threshold(4, (tiers[1]["alpha_s"], tiers[1]["beta_s_per_B"]), tree[:2], 2)
+    tp = [30e-6 + m / 12e9 for m in sizes]
+    ka, kb = CAL.p2p_scales(tiers[1], CAL.fit_p2p(sizes, tp)[:2])
+    sysm = CAL.system_from_tiers(tiers, flops_per_s=1e15, hbm_bytes=180 * W.GiB, tree_threshold=thr,
+                                 tree_chunks=2, p2p_alpha_scale=ka, p2p_beta_scale=kb, phi_pd=2.0)
+    r50 = M.resnet(50)
+    times = [(1e-4 * (i % 7 + 1), 2e-4 * (i % 5 + 1)) if r.kind == M.CONV else None for i, r in enumerate(r50.layers)]
+    em = CAL.empirical_model(r50, times, 1e15)
+    for sw in (W.config2(n_alpha=1, n_beta=1, b_list=[8, 64], pipe_smax=3), W.config5(s_max=3)):
+        sw.system = sysm
+        if sw.models[0].name.startswith("resnet50"):
+            sw.models = [em]
+        for sb in sw.subs:
+            sb.alpha, sb.beta = [], []
+        ctx = P.Context(0)
+        spec = ctx.prepare(sw)
+        osw = oracle_mod.OracleSweep(sw)
+        n = osw.size()
+        check_topk(ctx, spec, osw, 0, n, 64)
+        c = min(n, 200_000)
+        assert check_dense(ctx, spec, osw, 0, c, dev) == 0

@@ -37,12 +37,31 @@ def main():
             tiers.append(CAL.calibrate_tier(sizes, reps=20, group=g2))
         dist.barrier()
     tiers.append(CAL.calibrate_tier(sizes, reps=20))
+    # per-pattern parameters (SURVEY f2 / DESIGN.md Q40): small-message tree fit and its
+    # crossing with the ring form, point-to-point ping-pong (ranks 0, 1), ring Allgather
+    small = [1 << e for e in range(10, 19)]
+    t_small = CAL.time_allreduce(small, reps=20)
+    tree = CAL.fit_allreduce_tree(ws, small, t_small, k=1)
+    ring = (tiers[-1]["alpha_s"], tiers[-1]["beta_s_per_B"])
+    thr = CAL.tree_threshold(ws, ring, tree[:2], k=1)
+    t_p2p = CAL.time_p2p(sizes, reps=20)
+    p2p = CAL.fit_p2p(sizes, t_p2p)
+    ka, kb = CAL.p2p_scales(tiers[-1], p2p[:2])
+    t_ag = CAL.time_allgather([m // ws for m in sizes], reps=20)
+    ag = CAL.fit_allgather(ws, [m // ws for m in sizes], t_ag)
+    patterns = {"tree_alpha_s": tree[0], "tree_beta_s_per_B": tree[1], "tree_fit_rms_rel": tree[2],
+                "tree_threshold_B": thr, "small_sizes_B": small, "small_allreduce_s": t_small,
+                "p2p_alpha_s": p2p[0], "p2p_beta_s_per_B": p2p[1], "p2p_fit_rms_rel": p2p[2],
+                "p2p_alpha_scale": ka, "p2p_beta_scale": kb, "p2p_s": t_p2p,
+                "allgather_alpha_s": ag[0], "allgather_beta_s_per_B": ag[1], "allgather_fit_rms_rel": ag[2],
+                "allgather_s": t_ag}
     if rank == 0:
         m = M.resnet(50)
         times = CAL.time_layers(m, b=32, reps=10)
         R_ref = 1e15
         em = CAL.empirical_model(m, times, R_ref)
-        sysm = CAL.system_from_tiers(tiers, flops_per_s=R_ref, hbm_bytes=180 * W.GiB)
+        sysm = CAL.system_from_tiers(tiers, flops_per_s=R_ref, hbm_bytes=180 * W.GiB, tree_threshold=thr,
+                                     tree_chunks=1, p2p_alpha_scale=ka, p2p_beta_scale=kb)
         import paper_2104_09075_b200 as P
         sw = W.config2(n_alpha=1, n_beta=1, pipe_smax=min(4, ws))
         sw.models = [em]
@@ -65,7 +84,7 @@ def main():
                          "t_iter_s": pr.t_iter, "t_epoch_s": pr.t_epoch, "mem_GB": pr.mem / 1e9})
         rows = [{"name": r.name, "fw_s_per_sample": t[0], "bw_s_per_sample": t[1]}
                 for r, t in zip(m.layers, times) if t is not None]
-        res = {"world_size": ws, "device": torch.cuda.get_device_name(local), "tiers": tiers,
+        res = {"world_size": ws, "device": torch.cuda.get_device_name(local), "tiers": tiers, "patterns": patterns,
                "resnet50_layers_b32": rows, "effective_flops_per_s": em.meta["effective_flops_per_s"],
                "prediction": {"sweep": "cfg2 strategies on the calibrated system", "configs": ctx.sweep_size(spec),
                               "feasible": nf, "top": best}}

@@ -50,6 +50,143 @@ def fit_allreduce(p: int, sizes_bytes, times_s):
     return alpha, beta, rms
 
 
+def _lstsq_rel(A, t):
+    """Relative least squares (every sample weighs the same), non-negative alpha, positive beta."""
+    w = 1.0 / t
+    sol, *_ = np.linalg.lstsq(A * w[:, None], t * w, rcond=None)
+    alpha, beta = float(max(sol[0], 0.0)), float(max(sol[1], 1e-18))
+    pred = A @ np.array([alpha, beta])
+    return alpha, beta, float(np.sqrt(np.mean(((pred - t) / t) ** 2)))
+
+
+def fit_allreduce_tree(p: int, sizes_bytes, times_s, k: int = 1):
+    """Least-squares alpha, beta of the footnote's tree Allreduce form (Q18):
+    T = 2(ceil(log2 p) + k)(alpha + (m / (2k)) beta) -- NCCL's choice for small messages."""
+    if p < 2:
+        raise ValueError("an Allreduce fit needs p >= 2")
+    m = np.asarray(sizes_bytes, np.float64)
+    t = np.asarray(times_s, np.float64)
+    lg = 0
+    while (1 << lg) < p:
+        lg += 1
+    c = 2.0 * (lg + k)
+    return _lstsq_rel(np.stack([np.full_like(m, c), c * m / (2.0 * k)], axis=1), t)
+
+
+def tree_threshold(p: int, ring, tree, k: int = 1, lo: float = 1.0, hi: float = float(1 << 34)) -> float:
+    """Message size below which the fitted tree form predicts less time than the fitted ring
+    form (both forms of P:556 / P:559): the system's tree_threshold_B.  0 when the ring is never
+    slower in [lo, hi]; ring / tree = (alpha, beta) pairs."""
+    lg = 0
+    while (1 << lg) < p:
+        lg += 1
+
+    def t_ring(m):
+        return 2 * (p - 1) * (ring[0] + m / p * ring[1])
+
+    def t_tree(m):
+        return 2 * (lg + k) * (tree[0] + m / (2 * k) * tree[1])
+
+    if not t_tree(lo) < t_ring(lo):
+        return 0.0
+    if t_tree(hi) < t_ring(hi):
+        return hi
+    a, b = lo, hi
+    for _ in range(200):   # bisection on the crossing (both forms are affine in m)
+        mid = 0.5 * (a + b)
+        if t_tree(mid) < t_ring(mid):
+            a = mid
+        else:
+            b = mid
+    return b
+
+
+def fit_p2p(sizes_bytes, times_s):
+    """Hockney point-to-point alpha, beta (T_p2p(m) = alpha + m beta) from one-way times."""
+    m = np.asarray(sizes_bytes, np.float64)
+    t = np.asarray(times_s, np.float64)
+    return _lstsq_rel(np.stack([np.ones_like(m), m], axis=1), t)
+
+
+def fit_allgather(p: int, seg_bytes, times_s):
+    """Ring Allgather alpha, beta (T_ag = (p-1)(alpha + m_seg beta), per-PE segment, Q19)."""
+    if p < 2:
+        raise ValueError("an Allgather fit needs p >= 2")
+    m = np.asarray(seg_bytes, np.float64)
+    t = np.asarray(times_s, np.float64)
+    c = float(p - 1)
+    return _lstsq_rel(np.stack([np.full_like(m, c), c * m], axis=1), t)
+
+
+def p2p_scales(collective_tier: dict, p2p_fit) -> tuple:
+    """The system's p2p_alpha_scale / p2p_beta_scale (Q40): measured point-to-point
+    alpha, beta over the collective tier's (the paper plugs 'different network parameters ...
+    for MPI and NCCL', P:768-769)."""
+    a, b = p2p_fit[0], p2p_fit[1]
+    ca, cb = collective_tier["alpha_s"], collective_tier["beta_s_per_B"]
+    return (a / ca if ca > 0 else 1.0), (b / cb if cb > 0 else 1.0)
+
+
+def time_p2p(sizes_bytes, reps: int = 20, warmup: int = 3, device=None, group=None, peer=(0, 1)):
+    """One-way send time between two ranks of the group (half the median ping-pong round trip,
+    max over the pair); other ranks only join the final reduction."""
+    import torch
+    import torch.distributed as dist
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if torch.cuda.is_available() else torch.device("cpu"))
+    rank = dist.get_rank(group)
+    a_, b_ = peer
+    out = []
+    for m in sizes_bytes:
+        n = max(1, int(m) // 4)
+        buf = torch.ones(n, dtype=torch.float32, device=dev)
+        ts = []
+        for it in range(warmup + reps):
+            dist.barrier(group=group)
+            t0 = time.perf_counter()
+            if rank == a_:
+                dist.send(buf, dst=b_ if group is None else dist.get_global_rank(group, b_), group=group)
+                dist.recv(buf, src=b_ if group is None else dist.get_global_rank(group, b_), group=group)
+            elif rank == b_:
+                dist.recv(buf, src=a_ if group is None else dist.get_global_rank(group, a_), group=group)
+                dist.send(buf, dst=a_ if group is None else dist.get_global_rank(group, a_), group=group)
+            if dev.type == "cuda":
+                torch.cuda.synchronize()
+            if it >= warmup:
+                ts.append((time.perf_counter() - t0) / 2)
+        med = torch.tensor([statistics.median(ts) if rank in peer else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(med, op=dist.ReduceOp.MAX, group=group)
+        out.append(float(med.item()))
+    return out
+
+
+def time_allgather(seg_bytes, reps: int = 20, warmup: int = 3, device=None, group=None):
+    """Median all_gather time per per-PE segment size, max over the ranks."""
+    import torch
+    import torch.distributed as dist
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if torch.cuda.is_available() else torch.device("cpu"))
+    ws = dist.get_world_size(group)
+    out = []
+    for m in seg_bytes:
+        n = max(1, int(m) // 4)
+        buf = torch.ones(n, dtype=torch.float32, device=dev)
+        parts = [torch.empty_like(buf) for _ in range(ws)]
+        ts = []
+        for it in range(warmup + reps):
+            dist.barrier(group=group)
+            t0 = time.perf_counter()
+            dist.all_gather(parts, buf, group=group)
+            if dev.type == "cuda":
+                torch.cuda.synchronize()
+            if it >= warmup:
+                ts.append(time.perf_counter() - t0)
+        med = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(med, op=dist.ReduceOp.MAX, group=group)
+        out.append(float(med.item()))
+    return out
+
+
 def time_allreduce(sizes_bytes, reps: int = 20, warmup: int = 5, device=None, group=None):
     """Median wall time of dist.all_reduce per message size (float32 buffers), max over the
     ranks of the group.  CUDA tensors are timed with CUDA events on the current stream."""
