@@ -949,6 +949,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 j.s_lo = w.lo / nAB;
                 j.n = (w.hi + nAB - 1) / nAB - j.s_lo;
                 w.stab_lo = j.s_lo;
+                w.stab_n = j.n;
                 w.stab = reinterpret_cast<const PipeRec *>((uintptr_t)n_rec);   // offset until allocated
                 n_rec += j.n;
                 sjobs.push_back(j);
@@ -1001,10 +1002,11 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
                 const uint64_t nblk = range / (w.mode == 2 ? Q << ((w.flags & kWorkMaskS) ? kLowBitsSorted : 8) : Q);
-                // >= ~32 tiles per warp of this rank's shard (the last wave of a dynamic tile queue
-                // leaves at most one tile per warp unbalanced: <= ~3 %; measured 4 shards of cfg5
-                // at 16 per warp: 95 % efficiency); 1..256 partitions per lane per tile
-                uint64_t cper = nblk / n_shards / (32ull * warps * 32ull);
+                // >= ~16 tiles per warp of this rank's shard (the last wave of a dynamic tile queue
+                // leaves at most one tile per warp unbalanced; 4 shards of cfg5: 8.81 ms at 16 per
+                // warp, 8.94 ms at 32 -- the per-tile unranking and state rebuild cost more than
+                // the shorter tail); 1..256 partitions per lane per tile
+                uint64_t cper = nblk / n_shards / (32ull * warps * 16ull);
                 cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
                 w.steps = (uint32_t)cper;
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);

@@ -1512,6 +1512,30 @@ __device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) 
     m.pp_t = t.y;
 }
 
+// Software-pipelined structure records (A/B knob PARADL_REC_PREFETCH): the record after the
+// lane's current one is loaded while the current block is evaluated, so the step into the next
+// structure does not wait on L2.
+#ifndef PARADL_REC_PREFETCH
+#define PARADL_REC_PREFETCH 0
+#endif
+struct RecPF {
+    double4 q;
+    int2 t;
+};
+__device__ __forceinline__ void fetch_rec(const WorkItem &w, uint64_t s, RecPF &p) {
+    const PipeRec *r = w.stab + (s - w.stab_lo);
+    p.q = *reinterpret_cast<const double4 *>(r);
+    p.t = *reinterpret_cast<const int2 *>(&r->reason);
+}
+__device__ __forceinline__ void use_rec(const RecPF &p, Mid &m) {
+    m.comp = p.q.x;
+    m.pp_c = p.q.y;
+    m.pp_s = p.q.z;
+    m.I = p.q.w;
+    m.reason = (uint32_t)p.t.x;
+    m.pp_t = p.t.y;
+}
+
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
 // DENSE: 0 reduce (top-k / count), 1 dense writes, 2 compact writes (paradl_sweep_compact)
 template <int FAM, int DENSE>
@@ -1562,11 +1586,17 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         // pipeline reduce tiles read the structure terms from the structure table
         const bool rec = REC && w.stab != nullptr;
         uint64_t sidx = 0;   // rec: the lane's structure index
+#if PARADL_REC_PREFETCH
+        RecPF pf{};          // rec: the next structure's record, in flight
+#endif
         if ((uint32_t)lane < len) {
             decode(v, u0 + lane, L, cuts, cs);
             if (rec) {
                 sidx = struct_index(v, L);
                 load_rec(w, sidx, m);
+#if PARADL_REC_PREFETCH
+                if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
+#endif
             } else {
                 if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
                 if (LW) m.lwt = lw_base;
@@ -1801,7 +1831,12 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 if (alpha_i >= nA) {
                     alpha_i -= nA;
                     sidx++;
+#if PARADL_REC_PREFETCH
+                    use_rec(pf, m);
+                    if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
+#else
                     load_rec(w, sidx, m);
+#endif
                 }
             } else if (j < nsteps && (uint32_t)lane + 32u * j < len) {
                 // step into the next configuration: generic odometer (may leave the block)
@@ -1812,6 +1847,9 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     if (rec) {
                         sidx = struct_index(v, L);
                         load_rec(w, sidx, m);
+#if PARADL_REC_PREFETCH
+                        if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
+#endif
                     } else {
                         if (PIPE && lvl >= D_PART)
                             stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);

@@ -115,6 +115,7 @@ struct WorkItem {
                                    // [CmbN x (s_max+1)][CmbS x n_b(s_max+1)n_S][CmbD x n_b(s_max+1)n_dims]
     const struct PipeRec *stab;    // mode 0 pipeline, reduce: structure table (device global), else null
     uint64_t stab_lo;              // structure index of stab[0] within the sub-sweep
+    uint64_t stab_n;               // records in the structure table from stab_lo
 };
 
 // Structure record of a pipeline sub-sweep (reduce mode): the alpha/beta-invariant terms of
