@@ -13,8 +13,12 @@
  * rational (fractions.Fraction) evaluator, the per-layer literal fold
  * (or_eval_fold), Table 4 parameter counts and limits, degenerate identities.
  * Parity unpinned by the paper itself: the FLOP-based compute parametrisation
- * (Q28), gamma (Q22), the ds / pd compositions (Q16, Q17) -- pinned only by the
- * self-consistency checks above.  See DESIGN.md §2.4.
+ * (Q28), gamma (Q22), the ds / pd compositions (Q16, Q17), the per-layer strategy
+ * composition (LAYERWISE, Q39) and the p2p scales / pd, ds contention (Q40) -- pinned
+ * by the self-consistency checks above and by simulators the paper's primitives define
+ * (concurrent ring Allreduces for the pd exchange, with a link-level flow count for its
+ * contention; ring Allgather / Reduce-Scatter for the LAYERWISE strategy changes; all-D /
+ * all-F LAYERWISE == the Data / Filter rows bit for bit).  See DESIGN.md §2.4.
  */
 #include "oracle.h"
 
