@@ -580,8 +580,15 @@ def dominant_roofline(ctx, P, W, sweep, spec, stream, flush, my_hits, my_cnt, fp
     nf = int(my_cnt.item())
     opc = fp64_per_config(sweep.subs[di])
     ach = nf * opc / (ms * 1e-3) / 1e12
+    ncu_fp = None
+    try:
+        v = json.load(open(os.path.join(ROOT, "profiles", "fp64_ncu.json"))).get(sweep.name, {}).get(fam)
+        ncu_fp = float(v) if v is not None else None
+    except Exception:
+        pass
     return {"bound": "alu", "kernel": f"sweep_kernel<{fam.upper()},reduce>", "sub_sweep_configs": nd,
-            "launch_ms": ms, "fp64_inst_per_config": opc, "achieved": ach, "peak": fp64_peak / 1e12,
+            "launch_ms": ms, "fp64_inst_per_config": opc, "fp64_inst_per_config_ncu": ncu_fp,
+            "achieved": ach, "peak": fp64_peak / 1e12,
             "unit": "T fp64-pipe inst/s", "frac": ach / (fp64_peak / 1e12)}
 
 
