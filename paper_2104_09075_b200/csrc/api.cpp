@@ -347,10 +347,6 @@ static bool merge_level_off() {
 
 // A/B switch for experiments: PARADL_NO_COMB=1 keeps COMB pipeline / pd sweeps on mode 1
 // (tile_body_blocked) instead of mode 3 (tile_body_comb); same results
-static bool ws_off() {   // A/B switch: PARADL_NO_WS=1 keeps mode-3 sweeps in one warp (no mode 4)
-    static const bool off = getenv("PARADL_NO_WS") != nullptr;
-    return off;
-}
 static bool comb_off() {
     static const bool off = getenv("PARADL_NO_COMB") != nullptr;
     return off;
@@ -788,10 +784,6 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             h.radix[D_BETA] <= 2 && cmb_bytes <= (32u << 10) && !comb_off() &&
             smem + kLaneStateBytes + cmb_bytes + memo_n * sizeof(double) + 1024 <= c->smem_optin)
             mode = 3;
-        // mode 4: mode 3 split into producer / consumer warps (one pass of <= 4 S values)
-        if (mode == 3 && h.radix[D_S] <= 4 && !ws_off() &&
-            smem + kWsDtabBytes + cmb_bytes + memo_n * sizeof(double) + 1024 <= c->smem_optin)
-            mode = 4;
         // screened masks hold every stage quantity as an exact double: the model totals bound
         // each stage term, so they must stay below 2^53 (kWorkMaskD)
         bool maskd_ok = false;
@@ -837,7 +829,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 w.memo_n = (uint32_t)memo_n;
                 w.memo_off = a.memo_bytes;
                 a.memo_bytes += (uint32_t)align16(memo_n * sizeof(double));
-                if (mode == 3 || mode == 4) {
+                if (mode == 3) {
                     w.cmb_off = a.memo_bytes;
                     a.memo_bytes += (uint32_t)align16(cmb_bytes);
                     if (fam != PARADL_PD || P.subs[q].dims0_pow2) w.flags |= kWorkPow2;
@@ -893,7 +885,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     {
         const size_t n0 = L.size();
         for (size_t li = 0; li < n0; li++) {
-            LaunchArgs by_mode[5];
+            LaunchArgs by_mode[4];
             for (auto &x : by_mode) memset(&x, 0, sizeof x);
             for (int i = 0; i < L[li].n_work; i++) {
                 const WorkItem &w = L[li].work[i];
@@ -901,13 +893,13 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             }
             bool first = true;
             const uint32_t memo_bytes = L[li].memo_bytes, low_bytes = L[li].low_bytes, dtab_bytes = L[li].dtab_bytes;
-            for (int md = 0; md < 5; md++) {
+            for (int md = 0; md < 4; md++) {
                 LaunchArgs &x = by_mode[md];
                 if (x.n_work == 0) continue;
                 if (md) {
                     x.memo_bytes = memo_bytes;
                     x.low_bytes = low_bytes;
-                    x.dtab_bytes = md == 1 ? dtab_bytes : md == 3 ? kLaneStateBytes : md == 4 ? kWsDtabBytes : 0;
+                    x.dtab_bytes = md == 1 ? dtab_bytes : md == 3 ? kLaneStateBytes : 0;
                 } else if (fam_of[li] == PARADL_GPIPE) {
                     x.dtab_bytes = dtab_bytes;   // per-lane stage table
                 } else if (fam_of[li] == PARADL_DATA_LW) {
@@ -957,7 +949,6 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 j.s_lo = w.lo / nAB;
                 j.n = (w.hi + nAB - 1) / nAB - j.s_lo;
                 w.stab_lo = j.s_lo;
-                w.stab_n = j.n;
                 w.stab = reinterpret_cast<const PipeRec *>((uintptr_t)n_rec);   // offset until allocated
                 n_rec += j.n;
                 sjobs.push_back(j);
@@ -983,7 +974,7 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
     for (size_t li = 0; li < nl; li++) {
         LaunchArgs &a = L[li];
         if (smem + a.memo_bytes + a.low_bytes + a.dtab_bytes > c->smem_optin) {
-            if (fam_of[li] == PARADL_GPIPE || blk_of[li] >= 3)
+            if (fam_of[li] == PARADL_GPIPE || blk_of[li] == 3)
                 return fail(c, PARADL_ENOMEM, "image + per-lane tables exceed shared memory");
             a.dtab_bytes = 0;   // unscreened path
         }

@@ -1512,30 +1512,6 @@ __device__ __forceinline__ void load_rec(const WorkItem &w, uint64_t s, Mid &m) 
     m.pp_t = t.y;
 }
 
-// Software-pipelined structure records (A/B knob PARADL_REC_PREFETCH): the record after the
-// lane's current one is loaded while the current block is evaluated, so the step into the next
-// structure does not wait on L2.
-#ifndef PARADL_REC_PREFETCH
-#define PARADL_REC_PREFETCH 0
-#endif
-struct RecPF {
-    double4 q;
-    int2 t;
-};
-__device__ __forceinline__ void fetch_rec(const WorkItem &w, uint64_t s, RecPF &p) {
-    const PipeRec *r = w.stab + (s - w.stab_lo);
-    p.q = *reinterpret_cast<const double4 *>(r);
-    p.t = *reinterpret_cast<const int2 *>(&r->reason);
-}
-__device__ __forceinline__ void use_rec(const RecPF &p, Mid &m) {
-    m.comp = p.q.x;
-    m.pp_c = p.q.y;
-    m.pp_s = p.q.z;
-    m.I = p.q.w;
-    m.reason = (uint32_t)p.t.x;
-    m.pp_t = p.t.y;
-}
-
 // One tile (32*steps consecutive configurations of work item w) for the whole warp.
 // DENSE: 0 reduce (top-k / count), 1 dense writes, 2 compact writes (paradl_sweep_compact)
 template <int FAM, int DENSE>
@@ -1586,17 +1562,11 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
         // pipeline reduce tiles read the structure terms from the structure table
         const bool rec = REC && w.stab != nullptr;
         uint64_t sidx = 0;   // rec: the lane's structure index
-#if PARADL_REC_PREFETCH
-        RecPF pf{};          // rec: the next structure's record, in flight
-#endif
         if ((uint32_t)lane < len) {
             decode(v, u0 + lane, L, cuts, cs);
             if (rec) {
                 sidx = struct_index(v, L);
                 load_rec(w, sidx, m);
-#if PARADL_REC_PREFETCH
-                if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
-#endif
             } else {
                 if (PIPE) stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
                 if (LW) m.lwt = lw_base;
@@ -1831,12 +1801,7 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                 if (alpha_i >= nA) {
                     alpha_i -= nA;
                     sidx++;
-#if PARADL_REC_PREFETCH
-                    use_rec(pf, m);
-                    if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
-#else
                     load_rec(w, sidx, m);
-#endif
                 }
             } else if (j < nsteps && (uint32_t)lane + 32u * j < len) {
                 // step into the next configuration: generic odometer (may leave the block)
@@ -1847,9 +1812,6 @@ __device__ __forceinline__ void tile_body(const LaunchArgs &a, const WorkItem &w
                     if (rec) {
                         sidx = struct_index(v, L);
                         load_rec(w, sidx, m);
-#if PARADL_REC_PREFETCH
-                        if (sidx + 1 < w.stab_lo + w.stab_n) fetch_rec(w, sidx + 1, pf);
-#endif
                     } else {
                         if (PIPE && lvl >= D_PART)
                             stage_terms(v, L, cuts, cs, at<int64_t>(v.img, v.S->off_b)[L.d[D_B]], st);
@@ -2730,28 +2692,10 @@ static_assert(sizeof(CmbN) == 48 && sizeof(CmbS) == 32 && sizeof(CmbD) == 64, "c
 enum { LS_PRE = 0, LS_APRE = 6, LS_PRE2 = 12, LS_BPRE = 18, kLaneState = 24 };
 static_assert(kLaneStateBytes == kLaneState * 8u * kThreads, "lane state layout");
 
-// Mode 4 (warp-specialised mode 3): a producer warp computes every partition's record --
-// stage terms, comp per S, the 2 x 2 pipeline terms P, D(delta maxW), and what a re-evaluation
-// needs -- into a shared-memory slot; the paired consumer warp (lane i <-> lane i) turns it into
-// the partition's 128 keys and screens them.  The producer's integer work (stage terms,
-// successor, state rebuilds) then overlaps the consumer's FP64-bound key loop instead of
-// alternating with it in one warp.  One slot per pair, staged in registers on both sides;
-// named barriers FULL (producer -> consumer) and EMPTY (consumer -> producer), 64 threads.
-enum { RS_COMP = 0, RS_P = 4, RS_MW = 20, RS_ST = 21, RS_GBLK = 27, RS_PART = 28, RS_I0 = 29, RS_I1 = 30, RS_WI = 31,
-       kRecFields = 32 };
-constexpr int kPairs = kWarps / 2;
-constexpr uint32_t kSlotBytes = kRecFields * 8u * 32u;             // one record per lane, field-major
-constexpr uint32_t kWsLaneStride = kThreads / 2;                    // producer threads
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ int bar_full(int pair) { return 1 + pair; }
-__device__ __forceinline__ int bar_empty(int pair) { return 1 + kPairs + pair; }
-
-template <int FAM, int ROLE = 0>   // ROLE 0: whole partition in one warp; 1: producer of mode 4
+template <int FAM>
 __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
                                uint16_t *cuts, WarpTopK &tk, unsigned long long &cnt, const double *memo,
-                               int64_t *lstate, double *slot = nullptr, int wi = 0) {
-    constexpr int LSTRIDE = ROLE == 1 ? (int)kWsLaneStride : kThreads;
+                               int64_t *lstate) {
     BlkCtx C = make_blk(w, smem, memo);
     const View &v = C.v;
     const SubHdr *S = v.S;
@@ -2776,7 +2720,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const CmbS *tabS = reinterpret_cast<const CmbS *>(cb + ns1 * sizeof(CmbN));
     const CmbD *tabD =
         reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nS * sizeof(CmbS));
-    int64_t *ls = lstate + (ROLE == 1 ? threadIdx.x % kWsLaneStride : threadIdx.x);
+    int64_t *ls = lstate + threadIdx.x;
     const uint64_t nblk = (w.hi - w.lo) / C.Q;
     const uint64_t c = w.steps;
     const uint64_t blk0 = (tile * 32 + lane) * c;
@@ -2801,61 +2745,61 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 ns = L.ns;
                 if (ns >= 2) {
                     // a = c_{s-2} (row 0 if s = 2), b2 = c_{s-3} (row 0 if s <= 3)
-                    const int a0 = ns >= 3 ? cuts[(ns - 3) * LSTRIDE] : 0;
-                    const int b2 = ns >= 4 ? cuts[(ns - 4) * LSTRIDE] : 0;
+                    const int a0 = ns >= 3 ? cuts[(ns - 3) * kThreads] : 0;
+                    const int b2 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
                     StageT p2;
                     if (upd == 2) {   // maxima over stages 0..s-4 and the prefix values at b2
                         p2.maxF = p2.maxB = p2.maxU = p2.maxW = p2.maxY = p2.sumY = p2.memI = 0;
                         if (ns >= 4) stage_span(v, cuts, kThreads, twob, ns, 0, ns - 3, 0, p2);
-                        ls[(LS_PRE2 + 0) * LSTRIDE] = p2.maxF;
-                        ls[(LS_PRE2 + 1) * LSTRIDE] = p2.maxB;
-                        ls[(LS_PRE2 + 2) * LSTRIDE] = p2.maxU;
-                        ls[(LS_PRE2 + 3) * LSTRIDE] = p2.maxW;
-                        ls[(LS_PRE2 + 4) * LSTRIDE] = p2.memI;
-                        ls[(LS_PRE2 + 5) * LSTRIDE] = p2.maxY;
-                        ls[(LS_BPRE + 0) * LSTRIDE] = PF[b2];
-                        ls[(LS_BPRE + 1) * LSTRIDE] = PB[b2];
-                        ls[(LS_BPRE + 2) * LSTRIDE] = PU[b2];
-                        ls[(LS_BPRE + 3) * LSTRIDE] = PW[b2];
-                        ls[(LS_BPRE + 4) * LSTRIDE] = PX[b2];
-                        ls[(LS_BPRE + 5) * LSTRIDE] = PI[b2];
+                        ls[(LS_PRE2 + 0) * kThreads] = p2.maxF;
+                        ls[(LS_PRE2 + 1) * kThreads] = p2.maxB;
+                        ls[(LS_PRE2 + 2) * kThreads] = p2.maxU;
+                        ls[(LS_PRE2 + 3) * kThreads] = p2.maxW;
+                        ls[(LS_PRE2 + 4) * kThreads] = p2.memI;
+                        ls[(LS_PRE2 + 5) * kThreads] = p2.maxY;
+                        ls[(LS_BPRE + 0) * kThreads] = PF[b2];
+                        ls[(LS_BPRE + 1) * kThreads] = PB[b2];
+                        ls[(LS_BPRE + 2) * kThreads] = PU[b2];
+                        ls[(LS_BPRE + 3) * kThreads] = PW[b2];
+                        ls[(LS_BPRE + 4) * kThreads] = PX[b2];
+                        ls[(LS_BPRE + 5) * kThreads] = PI[b2];
                     } else {
-                        p2.maxF = ls[(LS_PRE2 + 0) * LSTRIDE];
-                        p2.maxB = ls[(LS_PRE2 + 1) * LSTRIDE];
-                        p2.maxU = ls[(LS_PRE2 + 2) * LSTRIDE];
-                        p2.maxW = ls[(LS_PRE2 + 3) * LSTRIDE];
-                        p2.memI = ls[(LS_PRE2 + 4) * LSTRIDE];
-                        p2.maxY = ls[(LS_PRE2 + 5) * LSTRIDE];
+                        p2.maxF = ls[(LS_PRE2 + 0) * kThreads];
+                        p2.maxB = ls[(LS_PRE2 + 1) * kThreads];
+                        p2.maxU = ls[(LS_PRE2 + 2) * kThreads];
+                        p2.maxW = ls[(LS_PRE2 + 3) * kThreads];
+                        p2.memI = ls[(LS_PRE2 + 4) * kThreads];
+                        p2.maxY = ls[(LS_PRE2 + 5) * kThreads];
                     }
                     // stage s-3 = rows (b2, a] (exists when s >= 3), folded into pre
                     const int64_t eF = PF[a0], eB = PB[a0], eU = PU[a0], eW = PW[a0], eX = PX[a0], eI = PI[a0];
                     if (ns >= 3) {
-                        const int64_t W3 = eW - ls[(LS_BPRE + 3) * LSTRIDE];
-                        p2.maxF = max(p2.maxF, eF - ls[(LS_BPRE + 0) * LSTRIDE]);
-                        p2.maxB = max(p2.maxB, eB - ls[(LS_BPRE + 1) * LSTRIDE]);
-                        p2.maxU = max(p2.maxU, eU - ls[(LS_BPRE + 2) * LSTRIDE]);
+                        const int64_t W3 = eW - ls[(LS_BPRE + 3) * kThreads];
+                        p2.maxF = max(p2.maxF, eF - ls[(LS_BPRE + 0) * kThreads]);
+                        p2.maxB = max(p2.maxB, eB - ls[(LS_BPRE + 1) * kThreads]);
+                        p2.maxU = max(p2.maxU, eU - ls[(LS_BPRE + 2) * kThreads]);
                         p2.maxW = max(p2.maxW, W3);
-                        p2.memI = max(p2.memI, twob * (eX - ls[(LS_BPRE + 4) * LSTRIDE]) + 2 * W3 +
-                                                   (eI - ls[(LS_BPRE + 5) * LSTRIDE]));
+                        p2.memI = max(p2.memI, twob * (eX - ls[(LS_BPRE + 4) * kThreads]) + 2 * W3 +
+                                                   (eI - ls[(LS_BPRE + 5) * kThreads]));
                         p2.maxY = max(p2.maxY, Y[a0 - 1]);
                     }
-                    ls[(LS_PRE + 0) * LSTRIDE] = p2.maxF;
-                    ls[(LS_PRE + 1) * LSTRIDE] = p2.maxB;
-                    ls[(LS_PRE + 2) * LSTRIDE] = p2.maxU;
-                    ls[(LS_PRE + 3) * LSTRIDE] = p2.maxW;
-                    ls[(LS_PRE + 4) * LSTRIDE] = p2.memI;
-                    ls[(LS_PRE + 5) * LSTRIDE] = p2.maxY;
-                    ls[(LS_APRE + 0) * LSTRIDE] = eF;
-                    ls[(LS_APRE + 1) * LSTRIDE] = eB;
-                    ls[(LS_APRE + 2) * LSTRIDE] = eU;
-                    ls[(LS_APRE + 3) * LSTRIDE] = eW;
-                    ls[(LS_APRE + 4) * LSTRIDE] = eX;
-                    ls[(LS_APRE + 5) * LSTRIDE] = eI;
-                    clast = cuts[(ns - 2) * LSTRIDE];
+                    ls[(LS_PRE + 0) * kThreads] = p2.maxF;
+                    ls[(LS_PRE + 1) * kThreads] = p2.maxB;
+                    ls[(LS_PRE + 2) * kThreads] = p2.maxU;
+                    ls[(LS_PRE + 3) * kThreads] = p2.maxW;
+                    ls[(LS_PRE + 4) * kThreads] = p2.memI;
+                    ls[(LS_PRE + 5) * kThreads] = p2.maxY;
+                    ls[(LS_APRE + 0) * kThreads] = eF;
+                    ls[(LS_APRE + 1) * kThreads] = eB;
+                    ls[(LS_APRE + 2) * kThreads] = eU;
+                    ls[(LS_APRE + 3) * kThreads] = eW;
+                    ls[(LS_APRE + 4) * kThreads] = eX;
+                    ls[(LS_APRE + 5) * kThreads] = eI;
+                    clast = cuts[(ns - 2) * kThreads];
                 }
                 upd = 0;
             }
-            PCHECK(ns == 1 || (clast >= 1 && clast <= G - 1 && clast > (ns >= 3 ? cuts[(ns - 3) * LSTRIDE] : 0)));
+            PCHECK(ns == 1 || (clast >= 1 && clast <= G - 1 && clast > (ns >= 3 ? cuts[(ns - 3) * kThreads] : 0)));
             if (ns == 1) {
                 st.maxF = PF[G] - PF[0];
                 st.maxB = PB[G] - PB[0];
@@ -2866,15 +2810,15 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 // stage s-2 = rows (a, c], stage s-1 = rows (c, G]
                 const int64_t cF = PF[clast], cB = PB[clast], cU = PU[clast], cW = PW[clast], cX = PX[clast],
                               cI = PI[clast], y = Y[clast - 1];
-                const int64_t W1 = cW - ls[(LS_APRE + 3) * LSTRIDE], W2 = PW[G] - cW;
-                st.maxF = max(ls[(LS_PRE + 0) * LSTRIDE], max(cF - ls[(LS_APRE + 0) * LSTRIDE], PF[G] - cF));
-                st.maxB = max(ls[(LS_PRE + 1) * LSTRIDE], max(cB - ls[(LS_APRE + 1) * LSTRIDE], PB[G] - cB));
-                st.maxU = max(ls[(LS_PRE + 2) * LSTRIDE], max(cU - ls[(LS_APRE + 2) * LSTRIDE], PU[G] - cU));
-                st.maxW = max(ls[(LS_PRE + 3) * LSTRIDE], max(W1, W2));
-                st.memI = max(ls[(LS_PRE + 4) * LSTRIDE],
-                              max(twob * (cX - ls[(LS_APRE + 4) * LSTRIDE]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * LSTRIDE]),
+                const int64_t W1 = cW - ls[(LS_APRE + 3) * kThreads], W2 = PW[G] - cW;
+                st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - ls[(LS_APRE + 0) * kThreads], PF[G] - cF));
+                st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - ls[(LS_APRE + 1) * kThreads], PB[G] - cB));
+                st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - ls[(LS_APRE + 2) * kThreads], PU[G] - cU));
+                st.maxW = max(ls[(LS_PRE + 3) * kThreads], max(W1, W2));
+                st.memI = max(ls[(LS_PRE + 4) * kThreads],
+                              max(twob * (cX - ls[(LS_APRE + 4) * kThreads]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * kThreads]),
                                   twob * (PX[G] - cX) + 2 * W2 + (PI[G] - cI)));
-                st.maxY = max(ls[(LS_PRE + 5) * LSTRIDE], y);
+                st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
             }
         }
         // ---- keys of the partition's S x dims x Ls x alpha x beta block
@@ -2923,29 +2867,6 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 P[u][2] = dmul(q.ppc, dadd(at1, x0));
                 P[u][3] = dmul(q.ppc, dadd(at1, x1));
             }
-            if constexpr (ROLE == 1) {
-                // hand the partition to the paired consumer lane (nS <= kSB: one pass)
-                bar_sync(bar_empty(threadIdx.x >> 5), 64);
-                double *r = slot + lane;
-#pragma unroll
-                for (int u = 0; u < kSB; u++) {
-                    r[(RS_COMP + u) * 32] = comp[u];
-#pragma unroll
-                    for (int q = 0; q < 4; q++) r[(RS_P + 4 * u + q) * 32] = P[u][q];
-                }
-                r[RS_MW * 32] = mW;
-                const int64_t stv[6] = {st.maxF, st.maxB, st.maxU, st.maxW, st.maxY, st.memI};
-#pragma unroll
-                for (int k = 0; k < 6; k++) r[(RS_ST + k) * 32] = __longlong_as_double(stv[k]);
-                r[RS_GBLK * 32] = __longlong_as_double((long long)(S->offset + w.lo + (blk0 + it) * C.Q));
-                r[RS_PART * 32] = __longlong_as_double((long long)L.part);
-                r[RS_I0 * 32] = __longlong_as_double((long long)((act ? 1ull : 0ull) | ((uint64_t)ns << 8) |
-                                                                 ((uint64_t)bi << 32)));
-                r[RS_I1 * 32] = __longlong_as_double((long long)(((uint64_t)L.d[D_FLOPS]) | ((uint64_t)L.d[D_CAP] << 32)));
-                r[RS_WI * 32] = __longlong_as_double((long long)wi);
-                bar_arrive(bar_full(threadIdx.x >> 5), 64);
-                continue;
-            }
             // per p_d value: the GE terms G = ge_c (alpha + ge_s beta) of the 2 x 2 rows, then the
             // 16 keys t = comp + G, t = t + P, key = t I and their smallest high word
             auto dims_keys = [&](const CmbD &d, double gs) {
@@ -2983,14 +2904,12 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             }
         }
         if (act && part_inf == 0.0) cnt += (unsigned long long)nSok * ndok * C.nLAB;
-        if constexpr (ROLE == 0) {
-            const bool maybe = act && hmin <= __double2hiint(tk.adm);
-            if (__any_sync(full, maybe)) {
-                const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
-                eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
-            }
-            tk.refresh();
+        const bool maybe = act && hmin <= __double2hiint(tk.adm);
+        if (__any_sync(full, maybe)) {
+            const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
+            eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
         }
+        tk.refresh();
         if (it + 1 < nmine) {
             if (ns >= 2 && clast < G - 1) {   // lexicographic successor moves only the last cut
                 clast++;
@@ -2998,124 +2917,26 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             } else if (ns >= 3 && L.part + 1 < S->part_n) {
                 // an earlier cut moves (same stage count: the last cut is at its maximum, so
                 // the successor is inside this stage-count block unless every cut is)
-                cuts[(ns - 2) * LSTRIDE] = (uint16_t)clast;
-                const int c3 = ns >= 4 ? cuts[(ns - 4) * LSTRIDE] : 0;
+                cuts[(ns - 2) * kThreads] = (uint16_t)clast;
+                const int c3 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
                 succ_comb(v, L, cuts, kThreads);
                 L.part++;
-                upd = (L.ns == ns && (ns < 4 || cuts[(ns - 4) * LSTRIDE] == c3)) ? 1 : 2;
+                upd = (L.ns == ns && (ns < 4 || cuts[(ns - 4) * kThreads] == c3)) ? 1 : 2;
             } else {
                 // a successor that moves c_{s-2} (same s, same slower digits, c_{s-3} kept)
                 // rebuilds pre from pre2 and one stage; anything else rebuilds both
-                if (ns >= 2) cuts[(ns - 2) * LSTRIDE] = (uint16_t)clast;
-                const int c3 = ns >= 4 ? cuts[(ns - 4) * LSTRIDE] : 0;
+                if (ns >= 2) cuts[(ns - 2) * kThreads] = (uint16_t)clast;
+                const int c3 = ns >= 4 ? cuts[(ns - 4) * kThreads] : 0;
                 const uint32_t d0 = L.d[D_B], d1 = L.d[D_FLOPS], d2 = L.d[D_CAP];
                 advance(w, v, L, cuts, kThreads);
                 const bool mid = ns >= 3 && L.ns == ns && L.d[D_B] == d0 && L.d[D_FLOPS] == d1 && L.d[D_CAP] == d2 &&
-                                 (ns < 4 || cuts[(ns - 4) * LSTRIDE] == c3);
+                                 (ns < 4 || cuts[(ns - 4) * kThreads] == c3);
                 upd = mid ? 1 : 2;
             }
         }
     }
 }
 
-
-// Mode-4 consumer: one record per lane from the paired producer -> the partition's keys (the
-// per-p_d loop of tile_body_comb, operation for operation), the screen, and (rarely) the exact
-// re-evaluation through eval_partition with the record's stage terms.  Returns false at the
-// producer's end marker.
-template <int FAM>
-__device__ bool comb_consume(const LaunchArgs &a, uint8_t *smem, const double *memo, WarpTopK &tk, const double *slot,
-                             int &wi_cached, BlkCtx &C) {
-    const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int pair = (threadIdx.x >> 5) - kPairs;
-    bar_sync(bar_full(pair), 64);
-    const double *r = slot + lane;
-    const int wi = (int)__double_as_longlong(r[RS_WI * 32]);
-    if (wi < 0) return false;
-    const WorkItem &w = a.work[wi];
-    if (wi != wi_cached) {
-        C = make_blk(w, smem, memo);
-        wi_cached = wi;
-    }
-    const SubHdr *S = C.v.S;
-    const uint32_t ns1 = (uint32_t)S->s_max + 1, nS = C.nS, nD = C.nD;
-    const uint8_t *cb = reinterpret_cast<const uint8_t *>(memo) + w.cmb_off;
-    const CmbD *tabD =
-        reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nS * sizeof(CmbS));
-    const uint64_t i0 = (uint64_t)__double_as_longlong(r[RS_I0 * 32]);
-    const bool act = i0 & 1ull;
-    const int ns = (int)((i0 >> 8) & 0xffffff);
-    const uint32_t bi = (uint32_t)(i0 >> 32);
-    double comp[kSB], P[kSB][4];
-#pragma unroll
-    for (int u = 0; u < kSB; u++) {
-        comp[u] = r[(RS_COMP + u) * 32];
-#pragma unroll
-        for (int q = 0; q < 4; q++) P[u][q] = r[(RS_P + 4 * u + q) * 32];
-    }
-    const double mW = r[RS_MW * 32];
-    const CmbD *drow = tabD + ((size_t)bi * ns1 + ns) * nD;
-    int hmin = 0x7fffffff;
-    auto dims_keys = [&](const CmbD &d, double gs) {
-        double Gq[4] = {0.0, 0.0, 0.0, 0.0};
-        if (FAM == PARADL_PD) {
-            const double g0 = dmul(gs, d.b0), g1 = dmul(gs, d.b1);
-            Gq[0] = dmul(d.gc, dadd(d.a0, g0));
-            Gq[1] = dmul(d.gc, dadd(d.a0, g1));
-            Gq[2] = dmul(d.gc, dadd(d.a1, g0));
-            Gq[3] = dmul(d.gc, dadd(d.a1, g1));
-        }
-#pragma unroll
-        for (int u = 0; u < kSB; u++) {
-            int h[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const double t = FAM == PARADL_PD ? dadd(dadd(comp[u], Gq[q]), P[u][q]) : dadd(comp[u], P[u][q]);
-                h[q] = __double2hiint(dmul(t, d.I));
-            }
-            hmin = min(hmin, min(min(h[0], h[1]), min(h[2], h[3])));
-        }
-    };
-    if (w.flags & kWorkPow2) {
-#pragma unroll kCombUnroll
-        for (uint32_t iD = 0; iD < nD; iD++) {
-            const CmbD d = drow[iD];
-            dims_keys(d, dmul(mW, d.scale));
-        }
-    } else {
-#pragma unroll 1
-        for (uint32_t iD = 0; iD < nD; iD++) {
-            const CmbD d = drow[iD];
-            dims_keys(d, d.div ? ddiv_rare(mW, i2d(d.pd)) : dmul(mW, d.scale));
-        }
-    }
-    const bool maybe = act && hmin <= __double2hiint(tk.adm);
-    if (__any_sync(full, maybe)) {
-        StageT st;
-        st.maxF = __double_as_longlong(r[(RS_ST + 0) * 32]);
-        st.maxB = __double_as_longlong(r[(RS_ST + 1) * 32]);
-        st.maxU = __double_as_longlong(r[(RS_ST + 2) * 32]);
-        st.maxW = __double_as_longlong(r[(RS_ST + 3) * 32]);
-        st.maxY = __double_as_longlong(r[(RS_ST + 4) * 32]);
-        st.memI = __double_as_longlong(r[(RS_ST + 5) * 32]);
-        st.sumY = 0;
-        Lane L;
-        const uint64_t i1 = (uint64_t)__double_as_longlong(r[RS_I1 * 32]);
-        for (int k = 0; k < kDigits; k++) L.d[k] = 0;
-        L.d[D_B] = bi;
-        L.d[D_FLOPS] = (uint32_t)(i1 & 0xffffffffu);
-        L.d[D_CAP] = (uint32_t)(i1 >> 32);
-        L.part = (uint64_t)__double_as_longlong(r[RS_PART * 32]);
-        L.ns = ns;
-        const uint64_t gblk = (uint64_t)__double_as_longlong(r[RS_GBLK * 32]);
-        unsigned long long dummy = 0;
-        eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, dummy);
-    }
-    bar_arrive(bar_empty(pair), 64);
-    tk.refresh();
-    return true;
-}
 // Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
 // with the same fp64 operations compute_mid uses, and the low-bit stage tables of mode 2.
 __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base, LowE *low_base) {
@@ -3159,7 +2980,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
         const int32_t *Sv = at<int32_t>(v.img, S->off_S);
         const int32_t *dmv = at<int32_t>(v.img, S->off_dims);
         const uint32_t nrow = S->radix[D_B] * (nS + nD);
-        if (w.family == PARADL_PD && (w.mode == 1 || w.mode == 3 || w.mode == 4)) {
+        if (w.family == PARADL_PD && (w.mode == 1 || w.mode == 3)) {
             // ring GE coefficient and tier per (stage count s, dims value): make_ar's ring
             // branch, ge_c = 2 (p_d - 1) (0 when p_d = 1), +inf when s p_d exceeds every tier
             const uint32_t nDp = nD + 1;
@@ -3188,7 +3009,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 }
             }
         }
-        if (w.mode == 3 || w.mode == 4) {
+        if (w.mode == 3) {
             // mode-3 tables (tile_body_comb): per stage count n the P2P tier's alpha/beta rows,
             // per (b, n, S) and (b, n, dims) the constants of eval_partition's trees
             const uint32_t ns1 = (uint32_t)S->s_max + 1, nb = S->radix[D_B];
@@ -3394,38 +3215,6 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
                                 : nullptr;
     if (BLK || FAM == PARADL_DATA_LW) build_memo(a, smem, memo, lowtab);
 
-    if constexpr (BLK == 4 && (FAM == PARADL_PIPELINE || FAM == PARADL_PD)) {
-        // mode 4: warps [0, kPairs) produce partition records, warps [kPairs, 2 kPairs) consume them
-        int64_t *lst = reinterpret_cast<int64_t *>(dtab);
-        double *slots = reinterpret_cast<double *>(dtab + kWsLaneStride * 24u);
-        if (warp < kPairs) {
-            double *slot = slots + (size_t)warp * (kSlotBytes / 8);
-            for (;;) {
-                unsigned long long t = 0;
-                if (lane == 0) t = atomicAdd(a.tile_counter, 1ull);
-                t = __shfl_sync(full, t, 0);
-                const uint64_t T = t * (uint64_t)a.n_shards + (uint64_t)a.shard;
-                if (T >= a.total_tiles) {
-                    bar_sync(bar_empty(warp), 64);
-                    slot[RS_WI * 32 + lane] = __longlong_as_double(-1ll);
-                    bar_arrive(bar_full(warp), 64);
-                    break;
-                }
-                int wi = 0;
-                while (wi + 1 < a.n_work && T >= a.work[wi + 1].tile_base) wi++;
-                tile_body_comb<FAM, 1>(a, a.work[wi], T - a.work[wi].tile_base, smem, cuts, tk, cnt, memo, lst,
-                                       slot, wi);
-            }
-        } else {
-            const double *slot = slots + (size_t)(warp - kPairs) * (kSlotBytes / 8);
-            bar_arrive(bar_empty(warp - kPairs), 64);   // the slot starts empty
-            int wi_cached = -1;
-            BlkCtx C;
-            while (comb_consume<FAM>(a, smem, memo, tk, slot, wi_cached, C)) {
-            }
-        }
-    } else
-
     for (;;) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(a.tile_counter, 1ull);
@@ -3438,7 +3227,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 2 ? PARADL_MINB + 1
         if (BLK == 1)
             tile_body_blocked<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo, dtab);
         else if (BLK == 3) {
-            if constexpr (FAM == PARADL_PIPELINE || FAM == PARADL_PD)
+            if (FAM == PARADL_PIPELINE || FAM == PARADL_PD)
                 tile_body_comb<FAM>(a, w, T - w.tile_base, smem, cuts, tk, cnt, memo,
                                     reinterpret_cast<int64_t *>(dtab));
         }
@@ -4137,14 +3926,12 @@ static void *sweep_fn(int family, int dense, int blk) {
         case PARADL_PIPELINE:
             return blk == 1   ? (void *)sweep_kernel<PARADL_PIPELINE, 0, 1>
                    : blk == 3 ? (void *)sweep_kernel<PARADL_PIPELINE, 0, 3>
-                   : blk == 4 ? (void *)sweep_kernel<PARADL_PIPELINE, 0, 4>
                               : (void *)sweep_kernel<PARADL_PIPELINE, 0, 2>;
         case PARADL_LAYERPURE:
             return blk == 1 ? (void *)sweep_kernel<PARADL_LAYERPURE, 0, 1> : (void *)sweep_kernel<PARADL_LAYERPURE, 0, 2>;
         case PARADL_PD:
             return blk == 1   ? (void *)sweep_kernel<PARADL_PD, 0, 1>
                    : blk == 3 ? (void *)sweep_kernel<PARADL_PD, 0, 3>
-                   : blk == 4 ? (void *)sweep_kernel<PARADL_PD, 0, 4>
                               : (void *)sweep_kernel<PARADL_PD, 0, 2>;
         default: return nullptr;
         }

@@ -33,9 +33,6 @@ constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 constexpr int kGpMax = PARADL_GPIPE_MAX_STAGES;
 // mode-3 (COMB, incremental stage terms) per-lane stage state: 24 int64 per thread, column layout
 constexpr uint32_t kLaneStateBytes = 24u * 8u * kThreads;
-// mode 4 (warp-specialised mode 3): producer lane state (half the threads) + one 32-field
-// record per lane for each of the kWarps/2 producer -> consumer pairs
-constexpr uint32_t kWsDtabBytes = 24u * 8u * (kThreads / 2) + (kWarps / 2) * 32u * 8u * 32u;
 // GPIPE per-lane stage table in shared memory: 4 doubles (f, g, m, u) per stage, column per thread
 constexpr uint32_t kGpipeTabBytes = 4u * kGpMax * 8u * kThreads;
 
@@ -118,7 +115,6 @@ struct WorkItem {
                                    // [CmbN x (s_max+1)][CmbS x n_b(s_max+1)n_S][CmbD x n_b(s_max+1)n_dims]
     const struct PipeRec *stab;    // mode 0 pipeline, reduce: structure table (device global), else null
     uint64_t stab_lo;              // structure index of stab[0] within the sub-sweep
-    uint64_t stab_n;               // records in the structure table from stab_lo
 };
 
 // Structure record of a pipeline sub-sweep (reduce mode): the alpha/beta-invariant terms of
