@@ -990,6 +990,9 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             c->occ_cache.push_back({okey, nb});
         }
         if (nb < 1) return fail(c, PARADL_ECUDA, "sweep kernel cannot be resident with %zu bytes of shared memory", smems[li]);
+        // A/B knob: PARADL_MAX_BPS=n caps the resident CTAs per SM (occupancy experiments)
+        static const int max_bps = getenv("PARADL_MAX_BPS") ? atoi(getenv("PARADL_MAX_BPS")) : 0;
+        if (max_bps > 0) nb = std::min(nb, max_bps);
         const int grid_max = c->n_sm * nb;
         const uint64_t warps = (uint64_t)grid_max * kWarps;
         uint64_t tiles = 0;
