@@ -2689,10 +2689,10 @@ struct __align__(16) CmbD {   // per (b, n, dims): ring GE coefficient (+inf: no
 static_assert(sizeof(CmbN) == 48 && sizeof(CmbS) == 32 && sizeof(CmbD) == 64, "comb table layout");
 
 // Per-lane stage state of tile_body_comb in shared memory (column per thread, int64):
-// pre = maxima over stages 0..s-3, pre2 = maxima over stages 0..s-4 (the "mid" successor,
-// which moves c_{s-2}, rebuilds pre from pre2 plus one stage).  Maxima: F, B, U, W, memI, Y.
-// The prefix values at a = c_{s-2} and b2 = c_{s-3} are read from the image's prefix arrays.
-enum { LS_PRE = 0, LS_PRE2 = 6, kLaneState = 12 };
+// pre = maxima over stages 0..s-3 and the prefix values at a = c_{s-2}; pre2 = maxima over
+// stages 0..s-4 and the prefix values at c_{s-3} (the "mid" successor, which moves c_{s-2},
+// rebuilds pre from pre2 plus one stage).  Maxima: F, B, U, W, memI, Y; prefixes: F, B, U, W, XY, BI.
+enum { LS_PRE = 0, LS_APRE = 6, LS_PRE2 = 12, LS_BPRE = 18, kLaneState = 24 };
 static_assert(kLaneStateBytes == kLaneState * 8u * kThreads, "lane state layout");
 
 template <int FAM>
@@ -2730,7 +2730,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const uint64_t nmine = blk0 < nblk ? min(c, nblk - blk0) : 0;
     const uint32_t iters = __reduce_max_sync(full, (uint32_t)nmine);
     Lane L;
-    int clast = 0, ns = 1, acut = 0;   // last cut c_{s-1}, a = c_{s-2}
+    int clast = 0, ns = 1;
     int upd = 2;   // stage state to rebuild before the next partition: 0 none, 1 mid, 2 all
     double cap_memo = CUDART_NAN;
     int64_t mem_max = -1;
@@ -2760,6 +2760,12 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                         ls[(LS_PRE2 + 3) * kThreads] = p2.maxW;
                         ls[(LS_PRE2 + 4) * kThreads] = p2.memI;
                         ls[(LS_PRE2 + 5) * kThreads] = p2.maxY;
+                        ls[(LS_BPRE + 0) * kThreads] = PF[b2];
+                        ls[(LS_BPRE + 1) * kThreads] = PB[b2];
+                        ls[(LS_BPRE + 2) * kThreads] = PU[b2];
+                        ls[(LS_BPRE + 3) * kThreads] = PW[b2];
+                        ls[(LS_BPRE + 4) * kThreads] = PX[b2];
+                        ls[(LS_BPRE + 5) * kThreads] = PI[b2];
                     } else {
                         p2.maxF = ls[(LS_PRE2 + 0) * kThreads];
                         p2.maxB = ls[(LS_PRE2 + 1) * kThreads];
@@ -2771,12 +2777,13 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                     // stage s-3 = rows (b2, a] (exists when s >= 3), folded into pre
                     const int64_t eF = PF[a0], eB = PB[a0], eU = PU[a0], eW = PW[a0], eX = PX[a0], eI = PI[a0];
                     if (ns >= 3) {
-                        const int64_t W3 = eW - PW[b2];
-                        p2.maxF = max(p2.maxF, eF - PF[b2]);
-                        p2.maxB = max(p2.maxB, eB - PB[b2]);
-                        p2.maxU = max(p2.maxU, eU - PU[b2]);
+                        const int64_t W3 = eW - ls[(LS_BPRE + 3) * kThreads];
+                        p2.maxF = max(p2.maxF, eF - ls[(LS_BPRE + 0) * kThreads]);
+                        p2.maxB = max(p2.maxB, eB - ls[(LS_BPRE + 1) * kThreads]);
+                        p2.maxU = max(p2.maxU, eU - ls[(LS_BPRE + 2) * kThreads]);
                         p2.maxW = max(p2.maxW, W3);
-                        p2.memI = max(p2.memI, twob * (eX - PX[b2]) + 2 * W3 + (eI - PI[b2]));
+                        p2.memI = max(p2.memI, twob * (eX - ls[(LS_BPRE + 4) * kThreads]) + 2 * W3 +
+                                                   (eI - ls[(LS_BPRE + 5) * kThreads]));
                         p2.maxY = max(p2.maxY, Y[a0 - 1]);
                     }
                     ls[(LS_PRE + 0) * kThreads] = p2.maxF;
@@ -2785,7 +2792,12 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                     ls[(LS_PRE + 3) * kThreads] = p2.maxW;
                     ls[(LS_PRE + 4) * kThreads] = p2.memI;
                     ls[(LS_PRE + 5) * kThreads] = p2.maxY;
-                    acut = a0;
+                    ls[(LS_APRE + 0) * kThreads] = eF;
+                    ls[(LS_APRE + 1) * kThreads] = eB;
+                    ls[(LS_APRE + 2) * kThreads] = eU;
+                    ls[(LS_APRE + 3) * kThreads] = eW;
+                    ls[(LS_APRE + 4) * kThreads] = eX;
+                    ls[(LS_APRE + 5) * kThreads] = eI;
                     clast = cuts[(ns - 2) * kThreads];
                 }
                 upd = 0;
@@ -2801,13 +2813,13 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 // stage s-2 = rows (a, c], stage s-1 = rows (c, G]
                 const int64_t cF = PF[clast], cB = PB[clast], cU = PU[clast], cW = PW[clast], cX = PX[clast],
                               cI = PI[clast], y = Y[clast - 1];
-                const int64_t W1 = cW - PW[acut], W2 = PW[G] - cW;
-                st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - PF[acut], PF[G] - cF));
-                st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - PB[acut], PB[G] - cB));
-                st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - PU[acut], PU[G] - cU));
+                const int64_t W1 = cW - ls[(LS_APRE + 3) * kThreads], W2 = PW[G] - cW;
+                st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - ls[(LS_APRE + 0) * kThreads], PF[G] - cF));
+                st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - ls[(LS_APRE + 1) * kThreads], PB[G] - cB));
+                st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - ls[(LS_APRE + 2) * kThreads], PU[G] - cU));
                 st.maxW = max(ls[(LS_PRE + 3) * kThreads], max(W1, W2));
                 st.memI = max(ls[(LS_PRE + 4) * kThreads],
-                              max(twob * (cX - PX[acut]) + 2 * W1 + (cI - PI[acut]),
+                              max(twob * (cX - ls[(LS_APRE + 4) * kThreads]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * kThreads]),
                                   twob * (PX[G] - cX) + 2 * W2 + (PI[G] - cI)));
                 st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
             }

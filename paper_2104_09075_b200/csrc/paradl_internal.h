@@ -31,8 +31,8 @@ constexpr uint32_t kMaskTabN = 72;              // per-stage-count tables of the
 constexpr uint32_t kMaxDtabBytes = 48u << 10;   // cap of the mode-1 per-lane dims tables
 constexpr int kMaxCuts = PARADL_MAX_COMB_CUTS;
 constexpr int kGpMax = PARADL_GPIPE_MAX_STAGES;
-// mode-3 (COMB, incremental stage terms) per-lane stage state: 12 int64 per thread, column layout
-constexpr uint32_t kLaneStateBytes = 12u * 8u * kThreads;
+// mode-3 (COMB, incremental stage terms) per-lane stage state: 24 int64 per thread, column layout
+constexpr uint32_t kLaneStateBytes = 24u * 8u * kThreads;
 // GPIPE per-lane stage table in shared memory: 4 doubles (f, g, m, u) per stage, column per thread
 constexpr uint32_t kGpipeTabBytes = 4u * kGpMax * 8u * kThreads;
 
