@@ -55,9 +55,10 @@ FP64_OPS_PER_CONFIG = {"pipeline": 4.0, "data": 4.0, "filter": 6.0 + 1 / M_SLOTS
 def fp64_per_config(sb) -> float:
     """Algorithmic FP64 instructions per feasible configuration of a sub-sweep.
     Pipeline / pd sub-sweeps with a small alpha x beta block run the lane-blocked screened
-    nest: per configuration t = comp + G, t += P, key = t * I (pd; pipeline has no G), with
-    G = ge_c (alpha + ge_s beta) shared by the 4 S values of a pass and P = pp_c (alpha +
-    pp_s beta) shared by the dims values; the admission screen is an integer min."""
+    nest: per configuration t = comp + G, t += P (pd; pipeline has no G), with G = ge_c (alpha
+    + ge_s beta) shared by the 4 S values of a pass and P = pp_c (alpha + pp_s beta) shared by
+    the dims values; the admission screen is an integer min of t's high word and one key = t * I
+    per pass (the key is monotone in t)."""
     from workloads import sweeps as W
     fam = W.FAMILY_NAMES[sb.family]
     nab = max(1, len(sb.alpha)) * max(1, len(sb.beta))
@@ -66,12 +67,14 @@ def fp64_per_config(sb) -> float:
         # canonical tree per mask, with what is invariant per stage count (cseg, pp_c, alpha,
         # beta) and per table entry (U tau, bS D(delta Y) beta: a maximum of monotone products
         # is the product of the maximum) hoisted exactly: D(maxF + maxB), x cseg, x tau,
-        # + U tau, alpha + Yb, x pp_c, comp + P2P, x I = 8 (DESIGN.md §5.1 mask blocks)
-        return 8.0
+        # + U tau, alpha + Yb, x pp_c, comp + P2P = 7; x I once per 512-mask block on the
+        # smallest t_iter (the key is monotone in t_iter; DESIGN.md §5.1 mask blocks)
+        return 7.0 + 1.0 / 512
     if fam in ("pd", "pipeline") and nab < 32:
         n_s, n_d = max(1, len(sb.S)), max(1, len(sb.dims))
         g = 3.0 * math.ceil(n_s / 4) / n_s if fam == "pd" else 0.0
-        return (3.0 if fam == "pd" else 2.0) + g + 3.0 / n_d
+        key = math.ceil(n_s / 4) / (n_s * nab)   # x I once per pass of 4 S x 4 alpha/beta rows
+        return (2.0 if fam == "pd" else 1.0) + key + g + 3.0 / n_d
     return float(FP64_OPS_PER_CONFIG[fam])
 
 

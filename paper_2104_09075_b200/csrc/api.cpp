@@ -794,7 +794,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
             maskd_ok = hm.FB < lim && hm.WU < lim && memb < lim && (__int128)c->sys.delta * hm.Ymax < lim;
         }
         // sorted 512-mask blocks (kWorkMaskS, tile_body_mask_s): one flops value, <= 4 tiers
-        const bool masks_ok = maskd_ok && h.radix[D_FLOPS] == 1 && c->sys.n_tiers <= 4 && !masks_off();
+        const bool masks_ok =
+            maskd_ok && h.radix[D_FLOPS] == 1 && h.radix[D_CAP] == 1 && c->sys.n_tiers <= 4 && !masks_off();
         const int low_bits = masks_ok ? kLowBitsSorted : 8;
         const uint64_t unit = mode == 2 ? Q << low_bits : Q;
         const uint64_t lo = r0 - s0, hi = r1 - s0;
@@ -845,8 +846,9 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 if (mode == 2) {
                     w.low_off = a.low_bytes / 64;
                     // 64-byte entries per b: LowE / LowD over 256 low masks, or (kWorkMaskS) the
-                    // sorted LowS table over 512
-                    a.low_bytes += h.radix[D_B] * (1u << low_bits) * 64u;
+                    // sorted LowS table over 512 followed by its per-(b, e, pop) feasible counts
+                    a.low_bytes += h.radix[D_B] * (1u << low_bits) * 64u +
+                                   (masks_ok ? (uint32_t)align16(h.radix[D_B] * (kLowBitsSorted + 1) * (kLowBitsSorted + 2) * 4u) : 0u);
                 }
             } else {
                 stride_digits(h, w);

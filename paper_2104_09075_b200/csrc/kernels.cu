@@ -2399,8 +2399,8 @@ __device__ void tile_body_mask_d(const LaunchArgs &a, const WorkItem &w, uint64_
 // Mode 2, sorted (kWorkMaskS: pipeline masks, one configuration per mask, one flops value, the
 // cfg3-ii shape).  Lanes own blocks of 2^kLowBitsS = 512 masks; the only per-CTA table is the
 // (e, pop)-sorted LowS (U tau and Ypp beta_t folded in, §5.1).  Per (e, pop) subgroup the stage
-// count, its tier and NTab row and the high part's P2P term are registers; per mask 8 fp64
-// operations and 5 compares.  A block whose screen passes (0.2 % of the work in cfg3-ii) forms
+// count, its tier and NTab row and the high part's P2P term are registers; per mask 7 fp64
+// operations (t_iter; x I once per block on the smallest t) and 5 compares.  A block whose screen passes (0.2 % of the work in cfg3-ii) forms
 // each mask's low stage terms from the prefix sums and re-evaluates it through eval_partition.
 template <int FAM>
 __device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_t tile, uint8_t *smem,
@@ -2439,7 +2439,7 @@ __device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_
         int c_h = G;
         int hpop = 0;
         int64_t b = 1;
-        int hmin = 0x7fffffff;
+        int hmin = 0x7fffffff, th = 0x7fffffff;
         uint32_t nok = 0;
         if (act) {
             b = at<int64_t>(v.img, v.S->off_b)[L.d[D_B]];
@@ -2481,6 +2481,8 @@ __device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_
             const NTab *nt = reinterpret_cast<const NTab *>(C.memo + (size_t)nb * (C.nS + C.nD)) +
                              (size_t)L.d[D_B] * kMaskTabN;
             const LowS *lsb = lows + ((size_t)L.d[D_B] << LB);
+            const uint32_t *fc = reinterpret_cast<const uint32_t *>(lows + ((size_t)nb << LB)) +
+                                 (size_t)L.d[D_B] * (LB + 1) * (LB + 2);
             const int64_t cF = PF[c_h], cB = PB[c_h], cU = PU[c_h], cW = PW[c_h], cX = PX[c_h], cI = PI[c_h];
             for (int e = 0; e <= LB; e++) {
                 // straddling stage (e, c_h] folded with the high stages
@@ -2494,7 +2496,10 @@ __device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_
                     const int tr = tier_by_n[ns];
                     const bool ok = grp_ok && tr >= 0;
                     const int tt = max(tr, 0);
-                    const double Ph = dmul(tq.ppc, dadd(tq.aw, dmul(hpps, tq.bw)));
+                    // an infeasible subgroup (memory of the high / straddling part, tier, S > b)
+                    // gets P_h = +inf: every key is +inf; memory-infeasible entries carry F = +inf
+                    const double Ph = ok ? dmul(tq.ppc, dadd(tq.aw, dmul(hpps, tq.bw))) : CUDART_INF;
+                    nok += ok ? fc[e * (LB + 2) + pop] : 0u;
                     const int j0 = kSub.start[e][pop], j1 = j0 + kSub.cnt[e][pop];
 #pragma unroll 2
                     for (int j = j0; j < j1; j++) {
@@ -2506,13 +2511,12 @@ __device__ void tile_body_mask_s(const LaunchArgs &a, const WorkItem &w, uint64_
                         const double Pl = dmul(tq.ppc, dadd(tq.aw, yb));
                         const double p2p = Pl > Ph ? Pl : Ph;
                         const double comp = dadd(dmul(dmul(tq.cseg, dadd(maxF, maxB)), tau), mUt);
-                        const double key = dmul(dadd(comp, p2p), I);
-                        const bool feas = ok & (qUM.y <= mem_max_d);
-                        nok += feas ? 1u : 0u;
-                        hmin = min(hmin, feas ? __double2hiint(key) : 0x7fffffff);
+                        th = min(th, __double2hiint(dadd(comp, p2p)));
                     }
                 }
             }
+            // key = t I is monotone in t: every key of the block is at least D(t_lo I)
+            hmin = __double2hiint(dmul(__hiloint2double(th, 0), I));
         }
         cnt += nok;
         const bool maybe = act && hmin <= __double2hiint(tk.adm);
@@ -2664,13 +2668,15 @@ __device__ void tile_body_mask(const LaunchArgs &a, const WorkItem &w, uint64_t 
 // the partition is infeasible) and the pipeline term P = pp_c (alpha + (bS D(delta maxY))
 // beta) for the <= 2 x 2 alpha/beta rows; per p_d value the GE term G = ge_c (alpha + ge_s
 // beta) with ge_s = D(delta maxW) / p_d (x 2^-k exactly for a power of two); per
-// configuration t = comp + G, t = t + P, key = t I.  The (b, stage count, S) and (b, stage
+// configuration t = comp + G, t = t + P (t_iter, exact); the screen forms key = t I once per
+// p_d value from the smallest t (below).  The (b, stage count, S) and (b, stage
 // count, p_d) constants -- cseg, pp_c, b/S, ge_c, I = D/(b p_d), the tiers' alpha/beta -- come
 // from per-CTA tables built with the memo (build_memo).  With one alpha (beta) row the second
 // is a duplicate of the first: duplicate keys cannot change a minimum.
 //
-// Selection.  Only the smallest high word of the partition's keys is kept (key <= adm implies
-// hi(key) <= hi(adm) for non-negative doubles); a partition that may hold a candidate is
+// Selection.  Only a lower bound of the high word of the partition's keys is kept (key <= adm
+// implies hi(key) <= hi(adm) for non-negative doubles; D(t I) is monotone in t, so the 16 keys
+// of one p_d value are at least D(t_lo I) with t_lo <= min t); a partition that may hold a candidate is
 // re-evaluated by eval_partition (offers, exact).  Memory feasibility is the integer
 // threshold memI <= mem_threshold(cap), exactly the fp64 compare (mem_threshold).  The feasible
 // count is separable: (#S <= b) x (#p_d with a tier) x n_LAB per feasible partition.
@@ -2881,16 +2887,20 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                     Gq[2] = dmul(d.gc, dadd(d.a1, g0));
                     Gq[3] = dmul(d.gc, dadd(d.a1, g1));
                 }
+                int th = 0x7fffffff;
 #pragma unroll
                 for (int u = 0; u < kSB; u++) {
                     int h[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const double t = FAM == PARADL_PD ? dadd(dadd(comp[u], Gq[q]), P[u][q]) : dadd(comp[u], P[u][q]);
-                        h[q] = __double2hiint(dmul(t, d.I));
+                        h[q] = __double2hiint(t);
                     }
-                    hmin = min(hmin, min(min(h[0], h[1]), min(h[2], h[3])));
+                    th = min(th, min(min(h[0], h[1]), min(h[2], h[3])));
                 }
+                // key = t I is monotone in t (I > 0): the smallest key of these 16 is at least
+                // D(t_lo I), t_lo = the smallest t with its low word cleared
+                hmin = min(hmin, __double2hiint(dmul(__hiloint2double(th, 0), d.I)));
             };
             if (w.flags & kWorkPow2) {   // every p_d a power of two: ge_s = mW 2^-k, no branch
 #pragma unroll kCombUnroll
@@ -3114,6 +3124,7 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
             const int64_t *Y = at<int64_t>(v.mb, M->off_y);
             const double tau = ddiv(1.0, at<double>(v.img, S->off_flops)[0]);
             const double *be = at<double>(v.img, S->off_beta);
+            const double mem_max_d = i2d(mem_threshold(v.H, at<double>(v.img, S->off_cap)[0]));
             LowS *ls = reinterpret_cast<LowS *>(low_base + w.low_off);
             const uint32_t n = S->radix[D_B] << kLowBitsS;
             for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
@@ -3139,7 +3150,21 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 q.Ut = dmul(i2d(U), tau);
                 q.M = i2d(Mm);
                 for (int t = 0; t < 4; t++) q.Yb[t] = t < v.H->n_ctiers ? dmul(Ypp, be[t + v.H->p2p_off]) : 0.0;
+                // one capacity (host-checked): a low part over it makes every mask of the entry
+                // infeasible -- its key becomes +inf through maxF and it is not counted
+                if (!(i2d(Mm) <= mem_max_d)) q.F = CUDART_INF;
                 ls[((size_t)ib << kLowBitsS) + lows_pos(x)] = q;
+            }
+            __syncthreads();
+            // memory-feasible entries per (b, e, pop) subgroup (one thread per subgroup)
+            uint32_t *fc = reinterpret_cast<uint32_t *>(ls + ((size_t)S->radix[D_B] << kLowBitsS));
+            constexpr int kE = kLowBitsS + 1, kP = kLowBitsS + 2;
+            for (uint32_t g = threadIdx.x; g < S->radix[D_B] * kE * kP; g += blockDim.x) {
+                const uint32_t ib = g / (kE * kP), e = (g / kP) % kE, pop = g % kP;
+                const int j0 = kSub.start[e][pop], j1 = j0 + kSub.cnt[e][pop];
+                uint32_t k = 0;
+                for (int j = j0; j < j1; j++) k += ls[((size_t)ib << kLowBitsS) + j].F != CUDART_INF;
+                fc[g] = k;
             }
         } else if (w.mode == 2) {
             const ModelHdr *M = v.M;
