@@ -778,7 +778,9 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         // mode 3 (tile_body_comb): COMB pipeline / pd with ring collectives and <= 2 x 2
         // alpha/beta rows -- incremental stage terms, per-(b, s, S) / (b, s, dims) tables
         const uint64_t ns1 = (uint64_t)h.s_max + 1;
-        const uint64_t cmb_bytes = ns1 * 48 + (uint64_t)h.radix[D_B] * ns1 * (h.radix[D_S] * 32ull + h.radix[D_DIMS] * 64ull);
+        // CmbS rows padded to whole passes of 4 S values (kSB in kernels.cu)
+        const uint64_t cmb_bytes =
+            ns1 * 48 + (uint64_t)h.radix[D_B] * ns1 * ((h.radix[D_S] + 3) / 4 * 4 * 32ull + h.radix[D_DIMS] * 64ull);
         if (mode == 1 && h.part_mode == PARADL_PART_COMB && (fam == PARADL_PIPELINE || fam == PARADL_PD) &&
             (fam == PARADL_PIPELINE || c->sys.tree_threshold_B <= 0.0) && h.radix[D_ALPHA] <= 2 &&
             h.radix[D_BETA] <= 2 && cmb_bytes <= (32u << 10) && !comb_off() &&

@@ -1175,11 +1175,15 @@ __device__ __forceinline__ bool hit_less(double ka, uint64_t ia, double kb, uint
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Sorted list of up to 64 (key, idx) entries held in registers across the warp:
-// lane l owns entries l (a) and l + 32 (b).  th = entry k-1 (the admission threshold).
+// Sorted list of up to 64 (key, idx) entries of one warp, kept in shared memory (the CTA's
+// merge buffer): lane l owns entries l (a) and l + 32 (b) and only ever touches those two, so
+// the warp's own program order is the only ordering needed.  insert / batch load the two
+// entries into registers, work on them with shuffles and store them back; the hot loops
+// carry only th = entry k-1 (the admission threshold) and the admission bound.
 struct WarpTopK {
-    double ka, kb, thk;
-    uint64_t ia, ib, thi;
+    paradl_hit *L;   // this warp's 64 entries (shared memory)
+    double thk;
+    uint64_t thi;
     int k;
     // Admission bound shared by every warp of the call: the k-th key of ANY full warp list
     // bounds the global k-th key (that warp alone holds k entries <= it), so configs with a
@@ -1189,12 +1193,31 @@ struct WarpTopK {
     unsigned long long *gbound;
     unsigned long long gnext;   // bound loaded at the previous refresh (software-pipelined load)
 
-    __device__ void init(int kk, unsigned long long *g = nullptr) {
+    __device__ void init(int kk, paradl_hit *list, unsigned long long *g = nullptr) {
+        const int lane = threadIdx.x & 31;
         k = kk;
-        ka = kb = thk = adm = CUDART_INF;
-        ia = ib = thi = ~0ull;
+        thk = adm = CUDART_INF;
+        thi = ~0ull;
         gbound = g;
         gnext = ~0ull;
+        L = list;
+        L[lane].idx = L[lane + 32].idx = ~0ull;
+        L[lane].key_epoch_s = L[lane + 32].key_epoch_s = CUDART_INF;
+        __syncwarp();
+    }
+    __device__ __forceinline__ void load(double &ka, uint64_t &ia, double &kb, uint64_t &ib) const {
+        const int lane = threadIdx.x & 31;
+        ka = L[lane].key_epoch_s;
+        ia = L[lane].idx;
+        kb = L[lane + 32].key_epoch_s;
+        ib = L[lane + 32].idx;
+    }
+    __device__ __forceinline__ void store(double ka, uint64_t ia, double kb, uint64_t ib) {
+        const int lane = threadIdx.x & 31;
+        L[lane].key_epoch_s = ka;
+        L[lane].idx = ia;
+        L[lane + 32].key_epoch_s = kb;
+        L[lane + 32].idx = ib;
     }
     // adopt the shared bound loaded at the previous call and issue the next load, so the
     // global-memory latency overlaps the work in between (whole warp; broadcast load)
@@ -1227,6 +1250,9 @@ struct WarpTopK {
     __device__ void insert(double key, uint64_t idx) {
         const int lane = threadIdx.x & 31;
         const unsigned full = 0xffffffffu;
+        double ka, kb;
+        uint64_t ia, ib;
+        load(ka, ia, kb, ib);
         int pos = __popc(__ballot_sync(full, hit_less(ka, ia, key, idx))) +
                   __popc(__ballot_sync(full, hit_less(kb, ib, key, idx)));
         if (pos >= k) return;
@@ -1253,6 +1279,7 @@ struct WarpTopK {
             kb = key;
             ib = idx;
         }
+        store(ka, ia, kb, ib);
         const int src = (k - 1) & 31;
         double tka = __shfl_sync(full, ka, src), tkb = __shfl_sync(full, kb, src);
         uint64_t tia = __shfl_sync(full, ia, src), tib = __shfl_sync(full, ib, src);
@@ -1294,6 +1321,9 @@ struct WarpTopK {
     __device__ void batch(double ck, uint64_t ci) {
         const int lane = threadIdx.x & 31;
         const unsigned full = 0xffffffffu;
+        double ka, kb;
+        uint64_t ia, ib;
+        load(ka, ia, kb, ib);
         sort32(ck, ci);
         const double rk = __shfl_sync(full, ck, 31 - lane);
         const uint64_t ri = __shfl_sync(full, ci, 31 - lane);
@@ -1315,6 +1345,7 @@ struct WarpTopK {
         }
         merge32(ka, ia);
         merge32(kb, ib);
+        store(ka, ia, kb, ib);
         const int src = (k - 1) & 31;
         const double tka = __shfl_sync(full, ka, src), tkb = __shfl_sync(full, kb, src);
         const uint64_t tia = __shfl_sync(full, ia, src), tib = __shfl_sync(full, ib, src);
@@ -2727,8 +2758,9 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const uint8_t *cb = reinterpret_cast<const uint8_t *>(memo) + w.cmb_off;
     const CmbN *tabN = reinterpret_cast<const CmbN *>(cb);
     const CmbS *tabS = reinterpret_cast<const CmbS *>(cb + ns1 * sizeof(CmbN));
+    const uint32_t nSp = (nS + kSB - 1) / kSB * kSB;   // CmbS rows padded to whole passes (sok = 0)
     const CmbD *tabD =
-        reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nS * sizeof(CmbS));
+        reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nSp * sizeof(CmbS));
     int64_t *ls = lstate + threadIdx.x;
     const uint64_t nblk = (w.hi - w.lo) / C.Q;
     const uint64_t c = w.steps;
@@ -2856,17 +2888,16 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
         }
         const double tau = C.tau;
-        const CmbS *srow = tabS + ((size_t)bi * ns1 + ns) * nS;
+        const CmbS *srow = tabS + ((size_t)bi * ns1 + ns) * nSp;
         const CmbD *drow = tabD + ((size_t)bi * ns1 + ns) * nD;
         int hmin = 0x7fffffff;
         uint32_t nSok = 0;
-        for (uint32_t iS0 = 0; iS0 < nS; iS0 += kSB) {
+        for (uint32_t iS0 = 0; iS0 < nSp; iS0 += kSB) {
             double comp[kSB], P[kSB][4];
 #pragma unroll
             for (int u = 0; u < kSB; u++) {
-                const uint32_t iS = iS0 + u < nS ? iS0 + u : nS - 1;
-                const CmbS q = srow[iS];
-                const bool sok = act && q.sok && iS0 + u < nS;
+                const CmbS q = srow[iS0 + u];
+                const bool sok = act && q.sok;
                 nSok += sok ? 1u : 0u;
                 comp[u] = dadd(dadd(dmul(dmul(q.cseg, FBs), tau), Utau), sok ? part_inf : INF);
                 const double pps = dmul(q.bS, dmaxY);
@@ -2922,7 +2953,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
             eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
         }
-        tk.refresh();
+        if ((it & 3) == 3) tk.refresh();   // the shared bound only tightens the screen
         if (it + 1 < nmine) {
             if (ns >= 2 && clast < G - 1) {   // lexicographic successor moves only the last cut
                 clast++;
@@ -3032,7 +3063,8 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
             uint8_t *cb = reinterpret_cast<uint8_t *>(memo_base) + w.cmb_off;
             CmbN *tn = reinterpret_cast<CmbN *>(cb);
             CmbS *ts = reinterpret_cast<CmbS *>(cb + ns1 * sizeof(CmbN));
-            CmbD *td = reinterpret_cast<CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)nb * ns1 * nS * sizeof(CmbS));
+            const uint32_t nSp = (nS + kSB - 1) / kSB * kSB;   // whole passes; padding rows sok = 0
+            CmbD *td = reinterpret_cast<CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)nb * ns1 * nSp * sizeof(CmbS));
             const uint32_t ia1 = nA > 1 ? 1 : 0, ib1 = nBt > 1 ? 1 : 0;
             for (uint32_t n = threadIdx.x; n < ns1; n += blockDim.x) {
                 const int t = n >= 1 ? tier_of(v.H, n) : -1;
@@ -3050,14 +3082,19 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 q.pad0 = q.pad1 = 0;
                 tn[n] = q;
             }
-            for (uint32_t e = threadIdx.x; e < nb * ns1 * nS; e += blockDim.x) {
-                const uint32_t ib = e / (ns1 * nS), n = (e / nS) % ns1, j = e % nS;
-                const int64_t b = bv[ib], Sg = Sv[j];
+            for (uint32_t e = threadIdx.x; e < nb * ns1 * nSp; e += blockDim.x) {
+                const uint32_t ib = e / (ns1 * nSp), n = (e / nSp) % ns1, j = e % nSp;
                 CmbS q;
-                q.bS = ddiv(i2d(b), i2d(Sg));
-                q.cseg = dmul(i2d((int64_t)n + Sg - 1), q.bS);
-                q.ppc = n > 1 ? i2d(2 * ((int64_t)n + Sg - 2)) : 0.0;
-                q.sok = Sg >= 1 && Sg <= b;
+                if (j < nS) {
+                    const int64_t b = bv[ib], Sg = Sv[j];
+                    q.bS = ddiv(i2d(b), i2d(Sg));
+                    q.cseg = dmul(i2d((int64_t)n + Sg - 1), q.bS);
+                    q.ppc = n > 1 ? i2d(2 * ((int64_t)n + Sg - 2)) : 0.0;
+                    q.sok = Sg >= 1 && Sg <= b;
+                } else {   // padding: comp = +inf, never counted
+                    q.bS = q.cseg = q.ppc = 0.0;
+                    q.sok = 0;
+                }
                 q.pad = 0;
                 ts[e] = q;
             }
@@ -3234,7 +3271,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 3 ? PARADL_COMB_MINB : BLK ==
     uint16_t *cuts = &ex->cuts[0][threadIdx.x];
     const unsigned full = 0xffffffffu;
     WarpTopK tk;
-    tk.init(a.k, DENSE ? nullptr : a.gbound);
+    tk.init(a.k, &ex->lists[warp][0], DENSE ? nullptr : a.gbound);
     unsigned long long cnt = 0;
     double *memo = reinterpret_cast<double *>(smem + a.img_bytes + sizeof(SmemExtra));
     LowE *lowtab = reinterpret_cast<LowE *>(smem + a.img_bytes + sizeof(SmemExtra) + a.memo_bytes);
@@ -3276,11 +3313,7 @@ __global__ void __launch_bounds__(kThreads, BLK == 3 ? PARADL_COMB_MINB : BLK ==
     if (!DENSE) {
         // CTA merge: the 8 warp lists (512 entries) are bitonic-sorted in shared memory and
         // the first k written out.
-        paradl_hit *lst = &ex->lists[0][0];
-        lst[warp * PARADL_MAX_TOPK + lane].idx = tk.ia;
-        lst[warp * PARADL_MAX_TOPK + lane].key_epoch_s = tk.ka;
-        lst[warp * PARADL_MAX_TOPK + lane + 32].idx = tk.ib;
-        lst[warp * PARADL_MAX_TOPK + lane + 32].key_epoch_s = tk.kb;
+        paradl_hit *lst = &ex->lists[0][0];   // the warp lists are already in place
         for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(full, cnt, o);
         if (lane == 0) atomicAdd(&s_count, cnt);
         __syncthreads();
@@ -3519,8 +3552,9 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
     }
     if (warp != 0) return;
     // pathological ties: one warp scans everything
+    __shared__ paradl_hit s_list[PARADL_MAX_TOPK];
     WarpTopK tk;
-    tk.init(k);
+    tk.init(k, s_list);
     {
         const int64_t n = n_lists * (int64_t)k;
         for (int64_t e = 0; e < n; e += 32) {
@@ -3530,14 +3564,8 @@ __global__ void __launch_bounds__(1024) merge_kernel(const paradl_hit *lists, in
             tk.offer(ok, ok ? lists[jj].key_epoch_s : CUDART_INF, ok ? lists[jj].idx : ~0ull);
         }
     }
-    if (out && lane < k) {
-        out[lane].idx = tk.ia;
-        out[lane].key_epoch_s = tk.ka;
-    }
-    if (out && lane + 32 < k) {
-        out[lane + 32].idx = tk.ib;
-        out[lane + 32].key_epoch_s = tk.kb;
-    }
+    if (out && lane < k) out[lane] = s_list[lane];
+    if (out && lane + 32 < k) out[lane + 32] = s_list[lane + 32];
     if (lane == 0 && count_out) *count_out = s_cnt;
     if (bound_out && tk.thi != ~0ull && lane == 0)
         atomicMin(bound_out, (unsigned long long)__double_as_longlong(tk.thk));
