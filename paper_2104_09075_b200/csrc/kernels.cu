@@ -2770,6 +2770,30 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
     Lane L;
     int clast = 0, ns = 1;
     int upd = 2;   // stage state to rebuild before the next partition: 0 none, 1 mid, 2 all
+    // the partition's StageT from the lane state: formed once for the keys and again, only
+    // when the screen passes, for the re-evaluation (so it is not live across the key block)
+    auto form_st = [&](StageT &st, int64_t twob) {
+        if (ns == 1) {
+            st.maxF = PF[G] - PF[0];
+            st.maxB = PB[G] - PB[0];
+            st.maxU = PU[G] - PU[0];
+            st.maxW = PW[G] - PW[0];
+            st.memI = twob * (PX[G] - PX[0]) + 2 * (PW[G] - PW[0]) + (PI[G] - PI[0]);
+        } else {
+            // stage s-2 = rows (a, c], stage s-1 = rows (c, G]
+            const int64_t cF = PF[clast], cB = PB[clast], cU = PU[clast], cW = PW[clast], cX = PX[clast],
+                          cI = PI[clast], y = Y[clast - 1];
+            const int64_t W1 = cW - ls[(LS_APRE + 3) * kThreads], W2 = PW[G] - cW;
+            st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - ls[(LS_APRE + 0) * kThreads], PF[G] - cF));
+            st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - ls[(LS_APRE + 1) * kThreads], PB[G] - cB));
+            st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - ls[(LS_APRE + 2) * kThreads], PU[G] - cU));
+            st.maxW = max(ls[(LS_PRE + 3) * kThreads], max(W1, W2));
+            st.memI = max(ls[(LS_PRE + 4) * kThreads],
+                          max(twob * (cX - ls[(LS_APRE + 4) * kThreads]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * kThreads]),
+                              twob * (PX[G] - cX) + 2 * W2 + (PI[G] - cI)));
+            st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
+        }
+    };
     double cap_memo = CUDART_NAN;
     int64_t mem_max = -1;
     if (nmine) decode(v, w.lo + blk0 * C.Q, L, cuts, kThreads);
@@ -2841,26 +2865,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 upd = 0;
             }
             PCHECK(ns == 1 || (clast >= 1 && clast <= G - 1 && clast > (ns >= 3 ? cuts[(ns - 3) * kThreads] : 0)));
-            if (ns == 1) {
-                st.maxF = PF[G] - PF[0];
-                st.maxB = PB[G] - PB[0];
-                st.maxU = PU[G] - PU[0];
-                st.maxW = PW[G] - PW[0];
-                st.memI = twob * (PX[G] - PX[0]) + 2 * (PW[G] - PW[0]) + (PI[G] - PI[0]);
-            } else {
-                // stage s-2 = rows (a, c], stage s-1 = rows (c, G]
-                const int64_t cF = PF[clast], cB = PB[clast], cU = PU[clast], cW = PW[clast], cX = PX[clast],
-                              cI = PI[clast], y = Y[clast - 1];
-                const int64_t W1 = cW - ls[(LS_APRE + 3) * kThreads], W2 = PW[G] - cW;
-                st.maxF = max(ls[(LS_PRE + 0) * kThreads], max(cF - ls[(LS_APRE + 0) * kThreads], PF[G] - cF));
-                st.maxB = max(ls[(LS_PRE + 1) * kThreads], max(cB - ls[(LS_APRE + 1) * kThreads], PB[G] - cB));
-                st.maxU = max(ls[(LS_PRE + 2) * kThreads], max(cU - ls[(LS_APRE + 2) * kThreads], PU[G] - cU));
-                st.maxW = max(ls[(LS_PRE + 3) * kThreads], max(W1, W2));
-                st.memI = max(ls[(LS_PRE + 4) * kThreads],
-                              max(twob * (cX - ls[(LS_APRE + 4) * kThreads]) + 2 * W1 + (cI - ls[(LS_APRE + 5) * kThreads]),
-                                  twob * (PX[G] - cX) + 2 * W2 + (PI[G] - cI)));
-                st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
-            }
+            form_st(st, twob);
         }
         // ---- keys of the partition's S x dims x Ls x alpha x beta block
         double FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, part_inf = INF;
@@ -2951,7 +2956,10 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
         const bool maybe = act && hmin <= __double2hiint(tk.adm);
         if (__any_sync(full, maybe)) {
             const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
-            eval_partition<FAM, false>(C, maybe, L, st, ns, gblk, tk, cnt);
+            StageT sr;
+            sr.maxF = sr.maxB = sr.maxU = sr.maxW = sr.maxY = sr.sumY = sr.memI = 0;
+            if (maybe) form_st(sr, 2 * bv[L.d[D_B]]);
+            eval_partition<FAM, false>(C, maybe, L, sr, ns, gblk, tk, cnt);
         }
         if ((it & 3) == 3) tk.refresh();   // the shared bound only tightens the screen
         if (it + 1 < nmine) {
