@@ -1008,11 +1008,21 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                 const uint64_t Q = (uint64_t)h.radix[D_ALPHA] * h.radix[D_BETA] * h.radix[D_LS] * h.radix[D_DIMS] *
                                    h.radix[D_S];
                 const uint64_t nblk = range / (w.mode == 2 ? Q << ((w.flags & kWorkMaskS) ? kLowBitsSorted : 8) : Q);
-                // >= ~16 tiles per warp of this rank's shard (the last wave of a dynamic tile queue
-                // leaves at most one tile per warp unbalanced; 4 shards of cfg5: 8.81 ms at 16 per
-                // warp, 8.94 ms at 32 -- the per-tile unranking and state rebuild cost more than
-                // the shorter tail); 1..256 partitions per lane per tile
-                uint64_t cper = nblk / n_shards / (32ull * warps * 16ull);
+                // Tiles per warp of this rank's shard: the last wave of a dynamic tile queue leaves
+                // at most one tile per warp unbalanced, and each tile pays a decode (unranking) and
+                // a stage-state rebuild; 1..256 partitions per lane per tile.
+                // 64 tiles per warp while a tile still holds >= 64 partitions (blocks) per lane,
+                // else 16 (COMB partitions: cfg5, session 16, 1 shard 28.5 -> 28.1 ms, 2 shards
+                // 14.86 -> 14.58 ms, 4 shards best at 16 per warp, 7.74 vs 7.94 ms at 32) or, for
+                // 512-mask blocks (cheap tiles), tiles of 64 blocks per lane (cfg3 196.7 -> 191.9
+                // ms); `ab_tiles_unrank_s16.log`.
+                // A/B knob: PARADL_TPW = a fixed number of tiles per warp instead
+                static const uint64_t tpw = getenv("PARADL_TPW") ? std::max(1, atoi(getenv("PARADL_TPW"))) : 0;
+                const uint64_t per = nblk / n_shards / (32ull * warps);
+                uint64_t cper = tpw ? per / tpw
+                                : per / 64 >= 64 ? per / 64
+                                : w.mode == 2 ? std::min<uint64_t>(64, per / 16)
+                                              : per / 16;
                 cper = std::max<uint64_t>(1, std::min<uint64_t>(cper, 256));
                 w.steps = (uint32_t)cper;
                 w.n_tiles = (nblk + 32ull * cper - 1) / (32ull * cper);
