@@ -780,10 +780,12 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
         const uint64_t ns1 = (uint64_t)h.s_max + 1;
         // CmbS rows padded to whole passes of 4 S values (kSB in kernels.cu)
         const uint64_t cmb_bytes =
-            ns1 * 48 + (uint64_t)h.radix[D_B] * ns1 * ((h.radix[D_S] + 3) / 4 * 4 * 32ull + h.radix[D_DIMS] * 64ull);
+            ns1 * 48 + (uint64_t)h.radix[D_B] * ns1 * ((h.radix[D_S] + 3) / 4 * 4 * 32ull + h.radix[D_DIMS] * 64ull) +
+            8ull * (h.radix[D_FLOPS] + h.radix[D_CAP]);   // + tau per flops value, memory threshold per cap
         if (mode == 1 && h.part_mode == PARADL_PART_COMB && (fam == PARADL_PIPELINE || fam == PARADL_PD) &&
             (fam == PARADL_PIPELINE || c->sys.tree_threshold_B <= 0.0) && h.radix[D_ALPHA] <= 2 &&
             h.radix[D_BETA] <= 2 && cmb_bytes <= (32u << 10) && !comb_off() &&
+            (uint64_t)h.radix[D_S] * h.radix[D_DIMS] * h.radix[D_LS] * h.radix[D_ALPHA] * h.radix[D_BETA] < (1ull << 31) &&
             smem + kLaneStateBytes + cmb_bytes + memo_n * sizeof(double) + 1024 <= c->smem_optin)
             mode = 3;
         // screened masks hold every stage quantity as an exact double: the model totals bound

@@ -2789,6 +2789,10 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
     const uint32_t nSp = (nS + kSB - 1) / kSB * kSB;   // CmbS rows padded to whole passes (sok = 0)
     const CmbD *tabD =
         reinterpret_cast<const CmbD *>(cb + ns1 * sizeof(CmbN) + (size_t)S->radix[D_B] * ns1 * nSp * sizeof(CmbS));
+    // per flops value tau = 1/R, per cap value the integer memory threshold (after CmbD)
+    const double *tauT = reinterpret_cast<const double *>(reinterpret_cast<const uint8_t *>(tabD) +
+                                                          (size_t)S->radix[D_B] * ns1 * nD * sizeof(CmbD));
+    const int64_t *memT = reinterpret_cast<const int64_t *>(tauT + S->radix[D_FLOPS]);
     int64_t *ls = lstate + threadIdx.x;
     const uint64_t nblk = (w.hi - w.lo) / C.Q;
     const uint64_t c = w.steps;
@@ -2822,8 +2826,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             st.maxY = max(ls[(LS_PRE + 5) * kThreads], y);
         }
     };
-    double cap_memo = CUDART_NAN;
-    int64_t mem_max = -1;
+    uint32_t tcnt = 0;   // feasible count of this tile (flushed into cnt before it could wrap)
     if (nmine) decode(v, w.lo + blk0 * C.Q, L, cuts, kThreads);
     for (uint32_t it = 0; it < iters; it++) {
         const bool act = it < nmine;
@@ -2899,28 +2902,19 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
         double FBs = 0.0, Utau = 0.0, dmaxY = 0.0, mW = 0.0, part_inf = INF;
         double at0 = 0.0, at1 = 0.0, bt0 = 0.0, bt1 = 0.0;
         uint32_t ndok = 0, bi = 0;
+        double tau = 0.0;
         if (act) {
-            const double cap = at<double>(v.img, S->off_cap)[L.d[D_CAP]];
-            const double R = at<double>(v.img, S->off_flops)[L.d[D_FLOPS]];
-            if (R != C.R_memo) {
-                C.R_memo = R;
-                C.tau = ddiv_rare(1.0, R);
-            }
-            if (!(cap == cap_memo)) {
-                cap_memo = cap;
-                mem_max = mem_threshold(H, cap);
-            }
+            tau = tauT[L.d[D_FLOPS]];
             bi = L.d[D_B];
             const CmbN tn = tabN[ns];
             at0 = tn.a0, at1 = tn.a1, bt0 = tn.b0, bt1 = tn.b1;
             ndok = (uint32_t)tn.ndok;
-            part_inf = (tn.ok && st.memI <= mem_max) ? 0.0 : INF;
+            part_inf = (tn.ok && st.memI <= memT[L.d[D_CAP]]) ? 0.0 : INF;
             FBs = i2d(st.maxF + st.maxB);
-            Utau = dmul(i2d(st.maxU), C.tau);
+            Utau = dmul(i2d(st.maxU), tau);
             dmaxY = i2d(delta * st.maxY);
             if (FAM == PARADL_PD) mW = i2d(delta * st.maxW);
         }
-        const double tau = C.tau;
         const CmbS *srow = tabS + ((size_t)bi * ns1 + ns) * nSp;
         const CmbD *drow = tabD + ((size_t)bi * ns1 + ns) * nD;
         int hmin = 0x7fffffff;
@@ -2980,7 +2974,13 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                 }
             }
         }
-        if (act && part_inf == 0.0) cnt += (unsigned long long)nSok * ndok * C.nLAB;
+        if (act && part_inf == 0.0) {
+            tcnt += nSok * ndok * C.nLAB;   // <= Q < 2^31 per partition (host check)
+            if (tcnt & 0x80000000u) {
+                cnt += tcnt;
+                tcnt = 0;
+            }
+        }
         const bool maybe = act && hmin <= __double2hiint(tk.adm);
         if (__any_sync(full, maybe)) {
             const uint64_t gblk = S->offset + w.lo + (blk0 + it) * C.Q;
@@ -3017,6 +3017,7 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             }
         }
     }
+    cnt += tcnt;
 }
 
 // Per-CTA prologue: memo tables of the lane-blocked work items (b/S and D/(b*dims0)),
@@ -3158,6 +3159,12 @@ __device__ void build_memo(const LaunchArgs &a, uint8_t *smem, double *memo_base
                 q.div = !pow2;
                 td[e] = q;
             }
+            double *tt = reinterpret_cast<double *>(td + (size_t)nb * ns1 * nD);
+            int64_t *mt = reinterpret_cast<int64_t *>(tt + S->radix[D_FLOPS]);
+            for (uint32_t e = threadIdx.x; e < S->radix[D_FLOPS]; e += blockDim.x)
+                tt[e] = ddiv(1.0, at<double>(v.img, S->off_flops)[e]);   // = eval_partition's tau
+            for (uint32_t e = threadIdx.x; e < S->radix[D_CAP]; e += blockDim.x)
+                mt[e] = mem_threshold(v.H, at<double>(v.img, S->off_cap)[e]);
         }
         if (w.mode == 2 && (w.flags & kWorkMaskD)) {
             // screened masks (n_S = 1, one alpha/beta row): per stage count n the same fp64
