@@ -2954,7 +2954,8 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
                         const double t = FAM == PARADL_PD ? dadd(dadd(comp[u], Gq[q]), P[u][q]) : dadd(comp[u], P[u][q]);
                         h[q] = __double2hiint(t);
                     }
-                    th = min(th, min(min(h[0], h[1]), min(h[2], h[3])));
+                    th = min(th, min(h[0], h[1]));   // two 3-input minima per S value
+                    th = min(th, min(h[2], h[3]));
                 }
                 // key = t I is monotone in t (I > 0): the smallest key of these 16 is at least
                 // D(t_lo I), t_lo = the smallest t with its low word cleared
