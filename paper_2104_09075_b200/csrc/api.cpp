@@ -852,7 +852,8 @@ static paradl_status run_sweep(paradl_ctx *c, const Plan &P, uint64_t first, uin
                     // 64-byte entries per b: LowE / LowD over 256 low masks, or (kWorkMaskS) the
                     // sorted LowS table over 512 followed by its per-(b, e, pop) feasible counts
                     a.low_bytes += h.radix[D_B] * (1u << low_bits) * 64u +
-                                   (masks_ok ? (uint32_t)align16(h.radix[D_B] * (kLowBitsSorted + 1) * (kLowBitsSorted + 2) * 4u) : 0u);
+                                   // (whole 64-byte units: low_off counts them)
+                                   (masks_ok ? (h.radix[D_B] * (kLowBitsSorted + 1) * (kLowBitsSorted + 2) * 4u + 63u) & ~63u : 0u);
                 }
             } else {
                 stride_digits(h, w);
