@@ -350,6 +350,33 @@ def test_mask_blocks_screened(dev, oracle_mod, seed, G, S):
         check_topk(ctx, spec, osw, a, c, rng.choice([7, 64]))
 
 
+@pytest.mark.parametrize("seed,G", [(35, 14), (36, 16)])
+def test_mask_sorted_tables_two_items(dev, oracle_mod, seed, G):
+    """Sorted mask path (one configuration per mask, one flops value, one capacity: the cfg3-ii
+    shape) with two b values in each of two work items: the per-CTA low tables of the items
+    sit one after the other (64-byte units), so the second item's table and the first
+    item's per-(b, e, pop) feasible counts must not overlap.  Whole sweep and windows."""
+    m = corpus.random_model(seed, G=G)
+    sysd = corpus.random_system(seed)
+    nt = len(sysd.tiers)
+    A = [[2e-6 * (t + 1) for t in range(nt)]]
+    Bt = [[3e-10 * (t + 1) for t in range(nt)]]
+    subs = [W.SubSweep(W.PIPELINE, part_mode=W.PART_MASK, b=[4, 16], S=[S], alpha=A, beta=Bt, cap=[2.0 ** 24])
+            for S in (2, 1)]
+    sw = W.Sweep([m], sysd, subs, "mask_sorted_two")
+    ctx = P.Context(0)
+    spec = ctx.prepare(sw)
+    osw = oracle_mod.OracleSweep(sw)
+    n = osw.size()
+    for k in (1, 64):
+        check_topk(ctx, spec, osw, 0, n, k)
+    rng = random.Random(seed)
+    for _ in range(3):
+        a = rng.randrange(n)
+        c = rng.randrange(1, n - a + 1)
+        check_topk(ctx, spec, osw, a, c, rng.choice([7, 64]))
+
+
 def test_unaligned_windows_all_families(dev, oracle_mod):
     """Ranges starting at every residue mod 32 (lane/slot alignment edge cases), cfg2 shapes."""
     sw = W.config2(n_alpha=3, n_beta=64, b_list=[2, 64], pipe_smax=2)
