@@ -2991,8 +2991,9 @@ __device__ void tile_body_comb(const LaunchArgs &a, const WorkItem &w, uint64_t 
             eval_partition<FAM, false>(C, maybe, L, sr, ns, gblk, tk, cnt);
         }
         // the shared bound only tightens the screen: every partition while the lists fill
-        // (the first ones pass the screen until the bound converges), then every 4th
-        if ((int)it < kRefreshWarm || (it & 3) == 3) tk.refresh();   // (warm-up: N = 256 shards 0.93 -> 0.63 ms)
+        // (the first ones pass the screen until the bound converges), then every 8th
+        // (`ab_refresh_period_s16.log`: every 2nd / 4th / 8th / 16th / 32nd)
+        if ((int)it < kRefreshWarm || (it & 7) == 7) tk.refresh();   // (warm-up: N = 256 shards 0.93 -> 0.63 ms)
         if (it + 1 < nmine) {
             if (ns >= 2 && clast < G - 1) {   // lexicographic successor moves only the last cut
                 clast++;
